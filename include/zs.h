@@ -1,0 +1,148 @@
+/*
+ * zs.h -- C ABI of the B200-native ZipGEMM library (libzs.so).
+ *
+ * Method: ZipServ / TCA-TBE (arxiv 2603.17435).  Citations: P:<line> = PAPER.md,
+ * S:<line> = SPEC.md (read while writing; nothing reads them at run time).
+ *
+ *   zs_encode        offline compressor, Alg. 1 with the layout of P:355-361
+ *                    and SPEC's ledger                              [host]
+ *   zs_decompress    ZipServ-Decomp: TCA-TBE -> BF16 in global memory
+ *                    using the decode of Alg. 2                     [device]
+ *   zs_gemm          ZipGEMM: Y = X * W^T with W streamed compressed and decoded per
+ *                    tile inside the kernel (north star)             [device]
+ *
+ * Notation: the paper writes Y = W X with W (M out x K) and X (K x N tokens).
+ * This ABI uses the F.linear convention: X is [M tokens][K], W is [N out][K], Y is [M][N].
+ *
+ * Conventions for every call
+ *   - Ownership: the caller owns every buffer.  The library never allocates device
+ *     memory and keeps no global mutable state (thread-safe for concurrent callers).
+ *   - Device calls are asynchronous on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream).  Validation is synchronous and happens before
+ *     launch; no exceptions cross the ABI.  Launch failures return ZS_ERR_CUDA.
+ *   - Encoded data is immutable after zs_encode and safe for concurrent readers.
+ *   - There is no CPU fallback: device entry points need an sm_100a GPU and return
+ *     ZS_ERR_UNSUPPORTED otherwise.
+ */
+#ifndef ZS_H_
+#define ZS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ZS_OK = 0,
+    ZS_ERR_INVALID_ARG = 1,   /* null pointer, non-positive dimension, bad base_exp */
+    ZS_ERR_SHAPE = 2,         /* M/N/K inconsistent with the encoded tensor        */
+    ZS_ERR_ALIGNMENT = 3,     /* pointer/stride violates the 16-byte TMA rule      */
+    ZS_ERR_UNSUPPORTED = 4,   /* no sm_100a device, or a size beyond the kernels   */
+    ZS_ERR_CORRUPT = 5,       /* offsets / segment sizes inconsistent       */
+    ZS_ERR_CUDA = 6,          /* a CUDA runtime call or kernel launch failed       */
+    ZS_ERR_CAPACITY = 7       /* caller buffer smaller than required               */
+} zs_status;
+
+/* Sizes of one encoded matrix.  Element counts unless suffixed _bytes / _words. */
+typedef struct {
+    int64_t rows, cols;                  /* logical N (out features), K (in features)      */
+    int64_t padded_rows, padded_cols;    /* multiples of 64 (BlockTile)      */
+    int64_t n_fragtiles;                 /* (padded_rows/8) * (padded_cols/8)             */
+    int64_t n_blocktiles;                /* (padded_rows/64) * (padded_cols/64)           */
+    int64_t h_bytes;                     /* PackedSignMantissa array, incl. 16-B padding   */
+    int64_t l_words;                     /* FullValue array (u16), incl. 16-B padding      */
+    int64_t max_h_seg_bytes;             /* largest per-BlockTile H segment (padded)       */
+    int64_t max_l_seg_bytes;             /* largest per-BlockTile L segment (padded)       */
+} zs_sizes;
+
+/*
+ * Non-owning view of an encoded matrix (all pointers host OR all device).
+ * Layout:
+ *   b1, b2, b3  one uint64 per 8x8 FragTile, bit p = codeword bit of the element at
+ *               position p = row*8 + col inside the FragTile (LSB first); b1 holds the
+ *               codeword LSB (Alg. 1 line 12).  FragTile order is canonical: BlockTile
+ *               (64x64) row-major -> TensorCoreTile (16x16) row-major -> FragTile
+ *               column-major in its 2x2 grid -> position ascending.
+ *   h           one byte (sign<<7 | mantissa) per in-window element, canonical order;
+ *               each BlockTile's segment starts 16-byte aligned and is zero padded.
+ *   l           one raw BF16 word per fallback element (codeword 000), same segmentation.
+ *   offsets     n_blocktiles + 1 pairs {h_start_bytes, l_start_bytes}; the last pair is a
+ *               sentinel = {h_bytes, 2*l_words}.  Both 16-byte aligned, non-decreasing.
+ *   base_exp    e_base = min(window) - 1 in [-1, 248], one per matrix.
+ *   pad_word    (0, base_exp+1, 0): the value stored in padded rows/columns.
+ * Decoding element p: if (b1|b2|b3) bit p is set, exponent = base_exp + codeword and
+ * sign/mantissa come from h[h_start + popc(M & ((1<<p)-1))]; else the word is
+ * l[l_start + p - popc(...)] (Alg. 2).
+ */
+typedef struct {
+    zs_sizes sz;
+    int32_t base_exp;
+    uint16_t pad_word;
+    uint16_t reserved;
+    const uint64_t *b1, *b2, *b3;
+    const uint8_t *h;
+    const uint16_t *l;
+    const uint64_t *offsets;
+} zs_tensor;
+
+/* Worst-case sizes for a rows x cols matrix (every element in H and in L). Host, O(1).
+ * Errors: ZS_ERR_INVALID_ARG if rows < 1, cols < 1 or upper == NULL. */
+zs_status zs_encode_bound(int64_t rows, int64_t cols, zs_sizes *upper);
+
+/* Phase I of Alg. 1: exponent histogram over the rows x cols LOGICAL
+ * elements of w (host, row-major, leading dimension ld >= cols), max-coverage window of
+ * 7 consecutive exponents (ties -> smallest start), base_exp = start - 1, and
+ * the exact sizes the encoding will need.  covered (may be NULL) = #elements in window.
+ * Errors: ZS_ERR_INVALID_ARG. */
+zs_status zs_encode_measure(const uint16_t *w, int64_t rows, int64_t cols, int64_t ld,
+                            int32_t *base_exp, int64_t *covered, zs_sizes *exact);
+
+/* Phase II of Alg. 1: encode w with the given base_exp (normally the one
+ * zs_encode_measure returned; a caller-forced base_exp is allowed, e.g. one window for a
+ * whole model).  Host buffers, caller-allocated with at least cap->... entries:
+ *   b1/b2/b3: cap->n_fragtiles, h: cap->h_bytes, l: cap->l_words,
+ *   offsets: 2 * (cap->n_blocktiles + 1).
+ * actual receives the sizes written.  Errors: ZS_ERR_INVALID_ARG (null, base_exp outside
+ * [-1, 248]), ZS_ERR_CAPACITY (a buffer too small; nothing beyond capacity is written). */
+zs_status zs_encode(const uint16_t *w, int64_t rows, int64_t cols, int64_t ld, int32_t base_exp,
+                    const zs_sizes *cap, uint64_t *b1, uint64_t *b2, uint64_t *b3,
+                    uint8_t *h, uint16_t *l, uint64_t *offsets,
+                    zs_sizes *actual, uint16_t *pad_word);
+
+/* ZipServ-Decomp: decode the DEVICE tensor w into out (device, row-major
+ * [w->sz.rows][ld_out] BF16, only the logical rows x cols are written), bit-exact.
+ * Errors: ZS_ERR_INVALID_ARG (null, ld_out < cols), ZS_ERR_UNSUPPORTED (no sm_100a),
+ * ZS_ERR_CUDA. */
+zs_status zs_decompress(const zs_tensor *w, uint16_t *out, int64_t ld_out, void *stream);
+
+/* Workspace (device bytes) zs_gemm needs for an M x N x K problem: fp32 split-K partial
+ * sums [M][N] plus per-band arrival counters.  The workspace must be zero-filled once
+ * before its first use; zs_gemm leaves it zero-filled again when it completes, so one
+ * workspace can be reused by every later call on the same stream. */
+size_t zs_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+
+/* ZipGEMM: Y[M][N] = X[M][K] * W[N][K]^T with fp32 accumulation in tensor
+ * memory and BF16 output (RNE).  x: device BF16, row-major, leading dimension ldx
+ * (elements), base 16-byte aligned and ldx*2 % 16 == 0 (TMA rule).  w: DEVICE tensor with
+ * w->sz.rows == N, w->sz.cols == K.  y: device BF16 [M][ldy], ldy >= N.  Outputs of
+ * padded rows are not written.  M >= 1 (any size; M > 256 is processed in 256-token
+ * chunks, each re-decoding W).  workspace: see zs_gemm_workspace_bytes.
+ * Errors: ZS_ERR_INVALID_ARG, ZS_ERR_SHAPE, ZS_ERR_ALIGNMENT, ZS_ERR_CAPACITY
+ * (workspace too small), ZS_ERR_UNSUPPORTED, ZS_ERR_CUDA. */
+zs_status zs_gemm(const uint16_t *x, int64_t ldx, const zs_tensor *w, uint16_t *y, int64_t ldy,
+                  int64_t M, int64_t N, int64_t K, void *workspace, size_t workspace_bytes,
+                  void *stream);
+
+/* Number of kernel launches the most recent successful zs_gemm / zs_decompress call on
+ * this thread issued (for the bench's gpu_launches count). */
+int zs_last_launch_count(void);
+
+/* Human-readable name of a status code (static storage). */
+const char *zs_status_string(zs_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZS_H_ */

@@ -1,0 +1,217 @@
+// zs_api.cu -- C ABI entry points of libzs.so (declared in include/zs.h).
+//
+// Validation happens synchronously before any launch; errors map to zs_status codes.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/zs.h"
+#include "zs_kernels.h"
+
+namespace {
+
+thread_local int g_last_launches = 0;
+
+inline int64_t up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct DevInfo {
+  int ok = 0;
+  int sms = 0;
+};
+
+zs_status device_check(int* sms) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return ZS_ERR_UNSUPPORTED;
+  int major = 0, minor = 0, n = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return ZS_ERR_CUDA;
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (major != 10 || minor != 0) return ZS_ERR_UNSUPPORTED;  // built for sm_100a only
+  *sms = n;
+  return ZS_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+zs_status validate_tensor(const zs_tensor* w) {
+  if (!w || !w->b1 || !w->b2 || !w->b3 || !w->offsets) return ZS_ERR_INVALID_ARG;
+  const zs_sizes& s = w->sz;
+  if (s.rows < 1 || s.cols < 1 || s.padded_rows != up(s.rows, 64) || s.padded_cols != up(s.cols, 64))
+    return ZS_ERR_SHAPE;
+  if (s.n_blocktiles != (s.padded_rows / 64) * (s.padded_cols / 64) || s.n_fragtiles != s.n_blocktiles * 64)
+    return ZS_ERR_CORRUPT;
+  if (s.max_h_seg_bytes < 0 || s.max_h_seg_bytes > 4096 || s.max_l_seg_bytes < 0 || s.max_l_seg_bytes > 8192 ||
+      (s.max_h_seg_bytes & 15) || (s.max_l_seg_bytes & 15))
+    return ZS_ERR_CORRUPT;
+  if ((s.h_bytes && !w->h) || (s.l_words && !w->l)) return ZS_ERR_INVALID_ARG;
+  if (w->base_exp < -1 || w->base_exp > 248) return ZS_ERR_INVALID_ARG;
+  if (!aligned16(w->b1) || !aligned16(w->b2) || !aligned16(w->b3) || !aligned16(w->offsets) ||
+      (w->h && !aligned16(w->h)) || (w->l && !aligned16(w->l)))
+    return ZS_ERR_ALIGNMENT;
+  return ZS_OK;
+}
+
+uint32_t eb7x2_of(int32_t base_exp) {
+  const uint32_t eb = (uint32_t)base_exp & 0xFFu;
+  return (eb << 7) | (eb << 23);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_tiled() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+}  // namespace
+
+extern "C" const char* zs_status_string(zs_status s) {
+  switch (s) {
+    case ZS_OK: return "ZS_OK";
+    case ZS_ERR_INVALID_ARG: return "ZS_ERR_INVALID_ARG";
+    case ZS_ERR_SHAPE: return "ZS_ERR_SHAPE";
+    case ZS_ERR_ALIGNMENT: return "ZS_ERR_ALIGNMENT";
+    case ZS_ERR_UNSUPPORTED: return "ZS_ERR_UNSUPPORTED";
+    case ZS_ERR_CORRUPT: return "ZS_ERR_CORRUPT";
+    case ZS_ERR_CUDA: return "ZS_ERR_CUDA";
+    case ZS_ERR_CAPACITY: return "ZS_ERR_CAPACITY";
+  }
+  return "ZS_ERR_UNKNOWN";
+}
+
+extern "C" int zs_last_launch_count(void) { return g_last_launches; }
+
+extern "C" zs_status zs_decompress(const zs_tensor* w, uint16_t* out, int64_t ld_out, void* stream) {
+  g_last_launches = 0;
+  zs_status st = validate_tensor(w);
+  if (st != ZS_OK) return st;
+  if (!out || ld_out < w->sz.cols) return ZS_ERR_INVALID_ARG;
+  int sms = 0;
+  if ((st = device_check(&sms)) != ZS_OK) return st;
+
+  zs::DecompParams p{};
+  p.b1 = w->b1;
+  p.b2 = w->b2;
+  p.b3 = w->b3;
+  p.h = w->h;
+  p.l = w->l;
+  p.offsets = w->offsets;
+  p.out = out;
+  p.ld_out = ld_out;
+  p.rows = w->sz.rows;
+  p.cols = w->sz.cols;
+  p.nbc = w->sz.padded_cols / 64;
+  p.n_blocktiles = w->sz.n_blocktiles;
+  p.hcap = (uint32_t)w->sz.max_h_seg_bytes + 16;
+  const uint32_t lcap = (uint32_t)w->sz.max_l_seg_bytes + 16;
+  p.stage_bytes = (uint32_t)up(1536 + p.hcap + lcap, 128);
+  p.eb7x2 = eb7x2_of(w->base_exp);
+  p.vec_ok = aligned16(out) && (ld_out % 8 == 0);
+  const size_t smem = zs::decompress_smem_bytes(p.stage_bytes);
+  int per_sm = (int)std::min<size_t>(8, (220 * 1024) / (smem + 1024));
+  per_sm = std::max(per_sm, 1);
+  const int64_t grid = std::min<int64_t>(p.n_blocktiles, (int64_t)sms * per_sm);
+  cudaError_t e = zs::launch_decompress(p, (int)grid, smem, (cudaStream_t)stream);
+  if (e != cudaSuccess) return ZS_ERR_CUDA;
+  g_last_launches = 1;
+  return ZS_OK;
+}
+
+extern "C" size_t zs_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+  (void)K;
+  if (M < 1 || N < 1) return 0;
+  const int64_t mc = std::min<int64_t>(M, 256);
+  const int64_t nbands = (up(N, 64) / 64 + 1) / 2;
+  return (size_t)(mc * N * 4) + (size_t)up(nbands * 4, 256);
+}
+
+extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w, uint16_t* y, int64_t ldy, int64_t M,
+                             int64_t N, int64_t K, void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  zs_status st = validate_tensor(w);
+  if (st != ZS_OK) return st;
+  if (!x || !y || M < 1 || N < 1 || K < 1) return ZS_ERR_INVALID_ARG;
+  if (N != w->sz.rows || K != w->sz.cols) return ZS_ERR_SHAPE;
+  if (ldx < K || ldy < N) return ZS_ERR_SHAPE;
+  if (!aligned16(x) || (ldx * 2) % 16 != 0) return ZS_ERR_ALIGNMENT;
+  if (!workspace || workspace_bytes < zs_gemm_workspace_bytes(M, N, K)) return ZS_ERR_CAPACITY;
+  if (!aligned16(workspace)) return ZS_ERR_ALIGNMENT;
+  int sms = 0;
+  if ((st = device_check(&sms)) != ZS_OK) return st;
+  auto enc = get_encode_tiled();
+  if (!enc) return ZS_ERR_UNSUPPORTED;
+
+  const int64_t mc_max = std::min<int64_t>(M, 256);
+  zs::GemmParams p{};
+  p.b1 = w->b1;
+  p.b2 = w->b2;
+  p.b3 = w->b3;
+  p.h = w->h;
+  p.l = w->l;
+  p.offsets = w->offsets;
+  p.y = y;
+  p.ldy = ldy;
+  p.ws = reinterpret_cast<float*>(workspace);
+  p.counters = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(workspace) + mc_max * N * 4);
+  p.N = N;
+  p.nbr = w->sz.padded_rows / 64;
+  p.nbc = w->sz.padded_cols / 64;
+  p.nbands = (p.nbr + 1) / 2;
+  p.total_units = p.nbands * p.nbc;
+  p.hcap = (uint32_t)w->sz.max_h_seg_bytes + 16;
+  p.lcap = (uint32_t)w->sz.max_l_seg_bytes + 16;
+  p.cslot_bytes = (uint32_t)up(3072 + 2 * (int64_t)p.hcap + 2 * (int64_t)p.lcap, 128);
+  p.eb7x2 = eb7x2_of(w->base_exp);
+
+  // X tensor map: dims {K, M}, row stride ldx*2 bytes, box {64, n_umma}, SWIZZLE_128B;
+  // out-of-bounds rows/columns are zero-filled by the TMA unit.
+  const int ngroups = zs::gemm_groups();
+  int launches = 0;
+  CUtensorMap xmap;
+  uint32_t cur_box = 0;
+  for (int64_t m0 = 0; m0 < M; m0 += 256) {
+    const int64_t mc = std::min<int64_t>(256, M - m0);
+    p.m0 = (int32_t)m0;
+    p.mc = (int32_t)mc;
+    p.n_umma = (uint32_t)up(mc, 16);
+    uint32_t tc = 32;
+    while (tc < 2 * p.n_umma) tc <<= 1;
+    p.tmem_cols = tc;
+    p.aslot_bytes = (uint32_t)up(16384 + (int64_t)p.n_umma * 128, 1024);
+    // compressed ring: largest multiple of the group count that fits in the smem budget
+    const size_t budget = 227 * 1024;
+    const size_t fixed = 1024 + 4096 + 1024 + (size_t)zs::gemm_aslots() * p.aslot_bytes;
+    if (fixed + (size_t)ngroups * p.cslot_bytes > budget) return ZS_ERR_UNSUPPORTED;
+    uint32_t ns = (uint32_t)((budget - fixed) / p.cslot_bytes);
+    ns = std::min<uint32_t>(ns, 16);
+    ns -= ns % ngroups;
+    p.n_cslots = ns;
+    if (p.n_umma != cur_box) {
+      cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+      cuuint64_t strides[1] = {(cuuint64_t)(ldx * 2)};
+      cuuint32_t box[2] = {64, p.n_umma};
+      cuuint32_t estr[2] = {1, 1};
+      CUresult r = enc(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(x), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return ZS_ERR_CUDA;
+      cur_box = p.n_umma;
+    }
+    const int64_t grid = std::min<int64_t>(p.total_units, sms);
+    cudaError_t e = zs::launch_gemm(p, xmap, (int)grid, zs::gemm_smem_bytes(p), (cudaStream_t)stream);
+    if (e != cudaSuccess) return ZS_ERR_CUDA;
+    ++launches;
+  }
+  g_last_launches = launches;
+  return ZS_OK;
+}

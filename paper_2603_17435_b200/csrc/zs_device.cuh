@@ -1,0 +1,270 @@
+// zs_device.cuh -- sm_100a device primitives shared by zs_decompress and zs_gemm.
+//
+// PTX wrappers (mbarrier, cp.async.bulk / TMA, tcgen05) and the branch-free TCA-TBE row
+// decoder.  Citations: P:<line> = PAPER.md, S:<line> = SPEC.md.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace zs {
+
+// ------------------------------------------------------------------ smem / mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// generic-proxy smem writes -> visible to the async proxy (tcgen05.mma operand reads)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ bulk copies (TMA)
+// 1-D bulk copy global -> shared, completion counted in bytes on `bar` (UBLKCP in SASS).
+// Requires 16-byte aligned addresses and a size that is a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// 2-D tiled TMA load (UTMALDG): box of the tensor map at coordinates (c0 inner, c1 outer).
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int32_t c0, int32_t c1, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
+// ------------------------------------------------------------------ tcgen05 / TMEM
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {  // whole warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+
+__device__ __forceinline__ void tmem_alloc_dyn(uint32_t* dst_smem, uint32_t cols) {  // whole warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {  // whole warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 inputs, fp32 accumulate), cta_group::1.
+__device__ __forceinline__ void umma_bf16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// 32 lanes x 32 bit, 16 consecutive columns per thread (thread i <-> TMEM lane base+i)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B canonical layout (8-row x 128-B
+// atoms stacked every 1024 B).  start must be inside a 1024-B aligned atom column.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);  // start address, 16-B units
+  d |= (uint64_t)1 << 16;                      // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;            // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                      // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                      // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, shape M x N.
+__host__ __device__ constexpr uint32_t umma_idesc_bf16(uint32_t M, uint32_t N) {
+  return (1u << 4)            // D format: f32
+         | (1u << 7)          // A format: bf16
+         | (1u << 10)         // B format: bf16
+         | ((N >> 3) << 17)   // N >> 3
+         | ((M >> 4) << 24);  // M >> 4
+}
+
+// ------------------------------------------------------------------ TCA-TBE row decoder
+//
+// The decode unit on sm_100a is one FragTile ROW: 8 consecutive K-elements of one weight
+// row = one byte of each bit-plane = one 16-byte chunk of the UMMA SW128 row.  It computes
+// exactly Alg. 2 for those 8 positions, amortised per row instead of per
+// element:
+//   M       = B1 | B2 | B3 restricted to the row's byte                   (Alg. 2 l.2)
+//   idx_H   = hs + popc(m & ((1<<i)-1))  -> PRMT byte selectors from a 256-entry table
+//   idx_L   = ls + i - popc(...)         -> PRMT selectors for the fallback merge
+//   e       = e_base + c, c = B3[p]B2[p]B1[p]                             (Alg. 2 l.15-16)
+//   word    = MakeBF16(sign, e, mantissa) or L[idx_L]                      (l.17 / l.21)
+// Both arms are computed for every element and merged by a byte permute: there is no
+// data-dependent branch on the common path.  Rows with >= 3 fallback
+// elements (rank >= 2) take a short patch loop (~0.05% of rows at r = 0.98).
+//
+// lut[m] (uint4): for output word j (elements 2j, 2j+1):
+//   bits  0..15  PRMT selector that pulls the H byte of element 2j into byte 0 and its
+//                sign-replicated copy into byte 1, likewise element 2j+1 into bytes 2, 3
+//   bits 16..31  PRMT selector over {Lpair, assembled word}: fallback elements of rank 0/1
+//                take L bytes (0,1)/(2,3), in-window elements keep their assembled half.
+__device__ __forceinline__ uint4 build_lut_entry(uint32_t m) {
+  uint32_t e[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t hs = 0, fs = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = 2 * j + h;
+      const uint32_t pre = __popc(m & ((1u << i) - 1u));  // set bits below i
+      const uint32_t rank = (uint32_t)i - pre;              // fallback rank of element i
+      hs |= (pre | ((pre | 8u) << 4)) << (8 * h);
+      uint32_t f;
+      if ((m >> i) & 1u)
+        f = (4u + 2u * h) | ((5u + 2u * h) << 4);  // keep assembled halfword h
+      else if (rank == 0)
+        f = 0u | (1u << 4);
+      else
+        f = 2u | (3u << 4);                         // rank 1 (rank >= 2 is patched)
+      fs |= f << (8 * h);
+    }
+    e[j] = hs | (fs << 16);
+  }
+  return make_uint4(e[0], e[1], e[2], e[3]);
+}
+
+// Decode one FragTile row.
+//   p1..p3   : the 64-bit bit-planes of the FragTile (lo/hi halves)
+//   r8       : row inside the FragTile (0..7) -> byte r8 of every plane
+//   H        : byte pointer to the BlockTile's PackedSignMantissa segment (smem)
+//   hs       : H index of the row's first in-window element (prefix popcount)
+//   L        : BlockTile's FullValue segment (smem); ls: L index of its first fallback
+//   eb7x2    : ((e_base mod 256) << 7) replicated in both halfwords
+// Returns 8 bf16 (element c in halfword c of the uint4, i.e. K order).
+__device__ __forceinline__ uint4 decode_row(uint64_t p1, uint64_t p2, uint64_t p3, uint32_t r8,
+                                            const uint8_t* __restrict__ H, uint32_t hs,
+                                            const uint16_t* __restrict__ L, uint32_t ls, const uint4* lut,
+                                            uint32_t eb7x2) {
+  const uint32_t sh = 8u * r8;
+  const uint32_t b1 = (uint32_t)(p1 >> sh) & 0xFFu;
+  const uint32_t b2 = (uint32_t)(p2 >> sh) & 0xFFu;
+  const uint32_t b3 = (uint32_t)(p3 >> sh) & 0xFFu;
+  const uint32_t m = b1 | b2 | b3;  // spatial indicator of the row
+  const uint4 ent = lut[m];
+
+  // 8 H bytes starting at hs (byte-granular window from three aligned words)
+  const uint32_t* H32 = reinterpret_cast<const uint32_t*>(H) + (hs >> 2);
+  const uint32_t hsh = (hs & 3u) * 8u;
+  const uint32_t w0 = H32[0], w1 = H32[1], w2 = H32[2];
+  const uint32_t hlo = __funnelshift_r(w0, w1, hsh);
+  const uint32_t hhi = __funnelshift_r(w1, w2, hsh);
+
+  // first two fallback values of the row
+  const uint32_t* L32 = reinterpret_cast<const uint32_t*>(L) + (ls >> 1);
+  const uint32_t lpair = __funnelshift_r(L32[0], L32[1], (ls & 1u) * 16u);
+
+  // codewords c_i = b3_i b2_i b1_i, two per 32-bit word (halfword h = element 2j+h)
+  uint32_t out[4];
+  const uint32_t sel[4] = {ent.x, ent.y, ent.z, ent.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t c0 = ((b1 >> (2 * j)) & 1u) | (((b2 >> (2 * j)) & 1u) << 1) | (((b3 >> (2 * j)) & 1u) << 2);
+    const uint32_t c1 =
+        ((b1 >> (2 * j + 1)) & 1u) | (((b2 >> (2 * j + 1)) & 1u) << 1) | (((b3 >> (2 * j + 1)) & 1u) << 2);
+    const uint32_t E = (c0 | (c1 << 16)) * 128u + eb7x2;        // (e_base + c) << 7 per half
+    const uint32_t P = __byte_perm(hlo, hhi, sel[j] & 0xFFFFu);  // s,s.. | mantissa bytes
+    const uint32_t asm_w = (P & 0x807F807Fu) | (E & 0x7F807F80u);
+    out[j] = __byte_perm(lpair, asm_w, sel[j] >> 16);
+  }
+
+  // rank >= 2 fallbacks (rare): patch from L directly
+  if (__popc(m) < 6) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t pre = __popc(m & ((1u << i) - 1u));
+      const uint32_t rank = (uint32_t)i - pre;
+      if (!((m >> i) & 1u) && rank >= 2) {
+        const uint32_t v = L[ls + rank];
+        const int j = i >> 1;
+        if (i & 1)
+          out[j] = (out[j] & 0x0000FFFFu) | (v << 16);
+        else
+          out[j] = (out[j] & 0xFFFF0000u) | v;
+      }
+    }
+  }
+  return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+}  // namespace zs

@@ -1,0 +1,62 @@
+// zs_kernels.h -- host-side launch interface of the sm_100a kernels (internal to libzs.so).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace zs {
+
+struct DecompParams {
+  const uint64_t* b1;
+  const uint64_t* b2;
+  const uint64_t* b3;
+  const uint8_t* h;
+  const uint16_t* l;
+  const uint64_t* offsets;  // n_blocktiles + 1 pairs
+  uint16_t* out;
+  int64_t ld_out;
+  int64_t rows, cols;
+  int64_t nbc;              // BlockTile columns
+  int64_t n_blocktiles;
+  uint32_t hcap, stage_bytes;
+  uint32_t eb7x2;
+  int vec_ok;
+};
+
+cudaError_t launch_decompress(const DecompParams& p, int grid, size_t smem, cudaStream_t stream);
+size_t decompress_smem_bytes(uint32_t stage_bytes);
+int decompress_threads();
+
+struct GemmParams {
+  const uint64_t* b1;
+  const uint64_t* b2;
+  const uint64_t* b3;
+  const uint8_t* h;
+  const uint16_t* l;
+  const uint64_t* offsets;
+  uint16_t* y;
+  int64_t ldy;
+  float* ws;                // [256][N] fp32 split-K partials (zero between calls)
+  uint32_t* counters;       // [nbands] arrival counters (zero between calls)
+  int64_t N;                // logical output features
+  int64_t nbr, nbc;         // BlockTile grid
+  int64_t nbands;           // ceil(nbr / 2): 128-row bands
+  int64_t total_units;      // nbands * nbc
+  int32_t m0, mc;           // token chunk [m0, m0 + mc)
+  uint32_t n_umma;          // mc rounded up to 16
+  uint32_t hcap, lcap;      // per-BlockTile segment capacities in smem
+  uint32_t cslot_bytes;     // compressed ring slot
+  uint32_t aslot_bytes;     // A (decoded) + X slot
+  uint32_t n_cslots;        // multiple of kGroups
+  uint32_t tmem_cols;
+  uint32_t eb7x2;
+};
+
+cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, size_t smem, cudaStream_t stream);
+size_t gemm_smem_bytes(const GemmParams& p);
+int gemm_threads();
+int gemm_groups();
+int gemm_aslots();
+
+}  // namespace zs

@@ -1,0 +1,192 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bars:
+  zs_decompress  bit-exact against the oracle's sequential decode AND the original weights.
+  zs_gemm        one-hot and integer pins: bit-exact; general inputs: err <= 1e-2 with
+                 err = max |Y - Y*| / (|X| |W|^T) (reading C15), against the fp64 oracle and
+                 against cuBLAS BF16 (torch F.linear) on the uncompressed weights.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import zs_inputs as G
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+
+
+@pytest.fixture(scope="module")
+def zs():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2603_17435_b200 as Z
+    Z.lib()
+    return Z
+
+
+DEV = "cuda:0"
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).to(DEV)
+
+
+def to_np(t):
+    return t.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16)
+
+
+def scaled_err(y, x, w, yref):
+    scale = np.abs(O.bf16_array_to_double(x)) @ np.abs(O.bf16_array_to_double(w)).T
+    return float(np.max(np.abs(y - yref) / np.maximum(scale, 1e-30)))
+
+
+# ----------------------------------------------------------------- zs_decompress
+DECOMP_CASES = {
+    "g256": lambda: G.gaussian_bf16(256, 256, 0.02, 1),
+    "specials_65x63": lambda: G.special_patterns(G.gaussian_bf16(65, 63, 0.02, 2), 0.05),
+    "specials_300x300_s0.1": lambda: G.special_patterns(G.gaussian_bf16(300, 300, 0.1, 3), 0.05),
+    "tiny_1x1": lambda: G.gaussian_bf16(1, 1, 0.02, 4),
+    "odd_7x9": lambda: G.gaussian_bf16(7, 9, 0.005, 5),
+    "all_patterns": G.all_patterns_256,
+    "all_zero": lambda: np.zeros((128, 192), np.uint16),
+    "realistic_1024x2048": lambda: G.realistic_bf16(1024, 2048, seed=6),
+}
+
+
+@pytest.mark.parametrize("case", sorted(DECOMP_CASES))
+def test_decompress_bit_exact(zs, case):
+    w = DECOMP_CASES[case]()
+    enc = zs.encode(w)
+    ref = O.encode(w)
+    assert enc.base_exp == ref.base_exp
+    got = to_np(zs.decompress(enc.to(DEV)))
+    np.testing.assert_array_equal(got, O.decode_sequential(ref))
+    np.testing.assert_array_equal(got, w)
+
+
+def test_decompress_forced_windows(zs):
+    w = G.gaussian_bf16(192, 320, 0.02, 8)
+    for be in (-1, 0, 60, 248):           # all-fallback, edge windows (C4)
+        enc = zs.encode(w, base_exp=be)
+        np.testing.assert_array_equal(to_np(zs.decompress(enc.to(DEV))), w)
+    w = np.full((64, 64), 0x7F80, np.uint16)
+    w[::3] = 0x7FC0                        # Inf/NaN in-window at base 248
+    np.testing.assert_array_equal(to_np(zs.decompress(zs.encode(w, base_exp=248).to(DEV))), w)
+
+
+def test_decompress_strided_output(zs):
+    w = G.gaussian_bf16(130, 100, 0.02, 9)
+    out = torch.full((130, 136), -1, dtype=torch.int16, device=DEV).view(torch.bfloat16)
+    zs.decompress(zs.encode(w).to(DEV), out=out[:, :100])
+    o = to_np(out)
+    np.testing.assert_array_equal(o[:, :100], w)
+    assert np.all(o[:, 100:] == 0xFFFF)
+
+
+def test_decompress_full_size_gateup(zs):
+    K, N = G.LAYERS["L8B.GateUp"]
+    w = G.gaussian_bf16(N, K, 0.02, G.seed_of("L8B.GateUp"))
+    enc = zs.encode(w)
+    got = to_np(zs.decompress(enc.to(DEV)))
+    assert np.array_equal(got, w)
+
+
+# ----------------------------------------------------------------- zs_gemm: exact pins
+def test_gemm_one_hot_layout(zs):
+    # X row m one-hot at column k_m -> Y[m][n] == W[n][k_m] exactly; 8 calls cover all K
+    N, K, M = 256, 256, 32
+    w = G.gaussian_bf16(N, K, 0.02, 11)
+    wd = zs.encode(w).to(DEV)
+    for call in range(K // M):
+        ks = [call * M + m for m in range(M)]
+        y = to_np(zs.gemm(to_dev(G.one_hot_activations(M, K, ks)), wd))
+        expect = w[:, ks].T
+        yf = G.bf16_bits_to_fp32(y)
+        np.testing.assert_array_equal(yf, G.bf16_bits_to_fp32(expect))
+
+
+@pytest.mark.parametrize("N,K,M", [(256, 256, 8), (1024, 4096, 32), (640, 1000, 17), (4096, 14336, 1),
+                                   (384, 512, 256), (256, 320, 300)])
+def test_gemm_integer_exact(zs, N, K, M):
+    w = G.integer_weights(N, K, seed=N + K)
+    x = G.integer_activations(M, K, seed=M)
+    y = to_np(zs.gemm(to_dev(x), zs.encode(w).to(DEV)))
+    exact = O.gemm_f64(x, w)
+    np.testing.assert_array_equal(y, O.round_bf16_array(exact))
+
+
+def test_gemm_identity_and_zero(zs):
+    K = 128
+    eye = np.zeros((K, K), np.uint16)
+    np.fill_diagonal(eye, 0x3F80)
+    x = G.activations_bf16(16, K, 3)
+    np.testing.assert_array_equal(to_np(zs.gemm(to_dev(x), zs.encode(eye).to(DEV))), x)
+    z = np.zeros((192, K), np.uint16)                       # e_base = -1 path
+    assert np.all(to_np(zs.gemm(to_dev(x), zs.encode(z).to(DEV))) & 0x7FFF == 0)
+
+
+# ----------------------------------------------------------------- zs_gemm: tolerance
+GEMM_SHAPES = [(256, 256, 8), (300, 200, 5), (1024, 1024, 1), (1024, 4096, 32), (2048, 4096, 64),
+               (4096, 4096, 128), (6144, 4096, 16), (512, 2048, 256), (320, 512, 513)]
+
+
+@pytest.mark.parametrize("N,K,M", GEMM_SHAPES)
+def test_gemm_vs_oracle_and_cublas(zs, N, K, M):
+    w = G.gaussian_bf16(N, K, 0.02, seed=N * 7 + K)
+    x = G.activations_bf16(M, K, seed=M + 1)
+    wd = zs.encode(w).to(DEV)
+    xt = to_dev(x)
+    y = zs.gemm(xt, wd)
+    yd = G.bf16_bits_to_fp32(to_np(y)).astype(np.float64)
+    yref = O.gemm_f64(x, w)
+    assert scaled_err(yd, x, w, yref) <= TOL
+    ycb = torch.nn.functional.linear(xt, to_dev(w)).float().cpu().numpy().astype(np.float64)
+    assert scaled_err(yd, x, w, ycb) <= TOL
+
+
+def test_gemm_realistic_weights(zs):
+    w = G.realistic_bf16(2048, 4096, seed=21)
+    x = G.activations_bf16(32, 4096, seed=22)
+    y = G.bf16_bits_to_fp32(to_np(zs.gemm(to_dev(x), zs.encode(w).to(DEV)))).astype(np.float64)
+    assert scaled_err(y, x, w, O.gemm_f64(x, w)) <= TOL
+
+
+@pytest.mark.parametrize("M", [1, 8, 32])
+def test_gemm_full_size_gateup_sampled(zs, M):
+    # BASELINE config 2 at full size, in the bench's launch configuration; outputs sampled
+    K, N = G.LAYERS["L8B.GateUp"]
+    w = G.gaussian_bf16(N, K, 0.02, G.seed_of("L8B.GateUp"))
+    x = G.activations_bf16(M, K, seed=G.seed_of("L8B.GateUp.X") + M)
+    wd = zs.encode(w).to(DEV)
+    y = G.bf16_bits_to_fp32(to_np(zs.gemm(to_dev(x), wd))).astype(np.float64)
+    cols = np.unique(np.concatenate([np.arange(0, N, 997), [0, 127, 128, N - 1]]))
+    yref = O.gemm_f64_cols(x, w, cols)
+    scale = np.abs(O.bf16_array_to_double(x)) @ np.abs(O.bf16_array_to_double(w[cols])).T
+    err = float(np.max(np.abs(y[:, cols] - yref) / scale))
+    assert err <= TOL
+
+
+def test_workspace_self_cleaning(zs):
+    w = G.gaussian_bf16(1024, 4096, 0.02, 31)
+    x = G.activations_bf16(24, 4096, 32)
+    ws = zs.workspace(24, 1024, 4096, DEV)
+    wd = zs.encode(w).to(DEV)
+    y1 = to_np(zs.gemm(to_dev(x), wd, ws=ws))
+    torch.cuda.synchronize()
+    assert int(ws.count_nonzero()) == 0
+    y2 = to_np(zs.gemm(to_dev(x), wd, ws=ws))
+    d = np.abs(G.bf16_bits_to_fp32(y1) - G.bf16_bits_to_fp32(y2))
+    assert d.max() <= 1e-2 * np.abs(G.bf16_bits_to_fp32(y1)).max()
+
+
+def test_gemm_errors(zs):
+    w = G.gaussian_bf16(128, 128, 0.02, 1)
+    wd = zs.encode(w).to(DEV)
+    with pytest.raises(zs.ZsError):
+        zs.gemm(to_dev(G.activations_bf16(4, 64, 1)), wd)          # K mismatch
+    x = torch.zeros((4, 136), dtype=torch.bfloat16, device=DEV)[:, 1:129]
+    with pytest.raises(zs.ZsError):
+        zs.gemm(x, wd)                                              # misaligned base (TMA rule)
