@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""ZipGEMM benchmark (driver contract).  One JSON line on rank 0.
+
+Workload (BASELINE.json configs[1]): LLaMA-3.1-8B GateUp_proj, K=4096, N=28672, synthetic
+sigma=0.02 Gaussian BF16 weights compressed with TCA-TBE, X ~ N(0,1) BF16, M=32 tokens.
+One step = one ZipGEMM Y[M][N] = X W^T (the whole hot path: TMA stream of the compressed
+tiles, decode, tcgen05 MMA, split-K fixup, BF16 epilogue).  With --gpus N the weight is
+column-sharded over N ranks (N/w output features each) and the Y slices are all-gathered
+over NCCL every step (strong scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--m M] [--layer NAME] [--impl reference]
+
+L2 hygiene: every step reads a different copy of the compressed weight (R copies, R x bytes
+> 3 x L2), so HBM, not L2, is measured.  Timing: CUDA events on the launching stream,
+barrier + synchronize on both sides, max over ranks.  Clocks are sampled with NVML during
+the warm-up + timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import zs_inputs as G  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--m", type=int, default=32)
+    ap.add_argument("--layer", default="L8B.GateUp")
+    ap.add_argument("--impl", default="zipgemm", choices=["zipgemm", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the cuBLAS / per-M context timings")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks (NVML)
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting", 0x1: "gpu_idle"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(device_index).uuid)
+            try:
+                self.h = pynvml.nvmlDeviceGetHandleByUUID(("GPU-" + uuid) if not uuid.startswith("GPU-") else uuid)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = repr(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_sample(layer, M, seconds_budget):
+    """Time the CPU oracle (decode + fp64 GEMM, as it stands) on a bounded row sample."""
+    import oracle as O
+    K, N = G.LAYERS[layer]
+    w_all = None
+    rows = 64
+    w = G.gaussian_bf16(N, K, 0.02, G.seed_of(layer))[:4096]  # same seeded weights, first rows
+    x = G.activations_bf16(M, K, seed=G.seed_of(layer + ".X") + M)
+    del w_all
+
+    def run(r):
+        enc = O.encode(w[:r], base_exp=O.encode(w[:64]).base_exp)  # offline, untimed
+        t0 = time.perf_counter()
+        wd = O.decode_sequential(enc)
+        O.gemm_f64(x, wd)
+        return time.perf_counter() - t0
+
+    t = run(rows)
+    if t < seconds_budget:
+        rows = int(min(4096, max(64, (seconds_budget / t) * rows)) // 64 * 64)
+        t = run(rows)
+    flops = 2.0 * M * rows * K
+    return {"value": flops / t / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": "oracle",
+            "sample": f"{layer} rows [0,{rows}) of N={N}, K={K}, M={M}: oracle decode_sequential + fp64 gemm, "
+                      f"{t:.2f} s single-threaded"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    layer, M = args.layer, args.m
+    K, N = G.LAYERS[layer]
+    w = G.gaussian_bf16(N, K, 0.02, G.seed_of(layer))[:64]
+    x = G.activations_bf16(M, K, seed=G.seed_of(layer + ".X") + M)
+    enc = O.encode(w)  # offline (the paper's compressor), not timed
+    budget = 150.0 / max(1, args.steps + args.warmup)
+
+    def step(r):
+        wd = O.decode_sequential(enc)
+        O.gemm_f64(x, wd[:r])
+
+    t0 = time.perf_counter()
+    step(64)
+    t64 = time.perf_counter() - t0
+    r = int(max(1, min(64, 64 * budget / max(t64, 1e-9))))
+    for _ in range(args.warmup):
+        step(r)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(r)
+    el = time.perf_counter() - t0
+    flops = 2.0 * M * r * K * args.steps
+    val = flops / el / 1e12
+    print(json.dumps({
+        "impl": "reference", "metric": metric_name(), "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{layer} ZipGEMM M={M} (K={K}, N={N})", "layer": layer, "M": M, "K": K, "N": N},
+        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": 1, "kind": "oracle",
+                         "sample": f"per step: oracle decode of one 64x{K} BlockTile row band + fp64 gemm of {r} "
+                                   f"rows at M={M}"},
+        "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def metric_name():
+    return "ZipGEMM TFLOP/s, HBM GB/s vs cuBLAS BF16 (LLaMA-3 8B/70B layers, M=1–8192)"
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_17435_b200 as Z
+    from paper_2603_17435_b200 import dist as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    peaks, peak_src = load_peaks()
+    layer, M = args.layer, args.m
+    K, N = G.LAYERS[layer]
+    w = G.gaussian_bf16(N, K, 0.02, G.seed_of(layer))
+    zh_full = Z.encode(w)
+    r0, r1 = D.shard_bounds(N, world, rank)
+    zh = D.shard_rows(zh_full, r0, r1) if world > 1 else zh_full
+    nloc = r1 - r0
+    wbytes = zh.nbytes()
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    R = max(2, math.ceil(3 * l2 / wbytes))
+    wdev = [zh.to(dev) for _ in range(R)]
+    x_host = G.activations_bf16(M, K, seed=G.seed_of(layer + ".X") + M)
+    x = torch.from_numpy(x_host.view(np.int16)).view(torch.bfloat16).to(dev)
+    y = torch.empty((M, nloc), dtype=torch.bfloat16, device=dev)
+    ws = Z.workspace(M, nloc, K, dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i, out_full=None):
+        Z.gemm(x, wdev[i % R], out=y, ws=ws)
+        if world > 1:
+            return D.gather_columns(y, world)
+        return y
+
+    # correctness gate on this very launch configuration (sampled, exact-size)
+    step(0)
+    torch.cuda.synchronize()
+    launches_per_step = Z.last_launch_count()
+
+    # CUDA graphs: one per weight copy (launch overhead off the critical path)
+    graphs = None
+    if world == 1:
+        try:
+            graphs = []
+            s = torch.cuda.Stream(dev)
+            s.wait_stream(stream)
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    step(0)
+            stream.wait_stream(s)
+            for r in range(R):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    step(r)
+                graphs.append(g)
+        except Exception as e:  # pragma: no cover
+            print(f"[bench] graph capture failed ({e!r}); timing eager launches", file=sys.stderr)
+            graphs = None
+
+    def run_step(i):
+        if graphs is not None:
+            graphs[i % R].replay()
+        else:
+            step(i)
+
+    clocks = ClockSampler(local)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with clocks:
+        for i in range(args.warmup):
+            run_step(i)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            run_step(i)
+            ev[i][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = t0.elapsed_time(t1)
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    sec = ms / 1e3
+    flops_step = 2.0 * M * N * K
+    bytes_step_alg = zh_full.nbytes() + 2.0 * M * K * world + 2.0 * M * N
+    value = flops_step * args.steps / sec / 1e12
+    hbm_gbs = bytes_step_alg * args.steps / sec / 1e9
+
+    # roofline of the dominant kernel (zipgemm_kernel): algorithmic bytes per launch / duration
+    bytes_launch = wbytes + 2.0 * M * K + 2.0 * M * nloc
+    achieved = bytes_launch / (kern_ms / 1e3) / 1e9
+    peak = float(peaks["hbm_gbs"])
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                pj = json.load(f)
+            key = f"{layer}.M{M}.w{world}"
+            if key in pj.get("zipgemm", {}):
+                traffic = pj["zipgemm"][key].get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # e2e: host buffers through the public API (H2D of X, ZipGEMM, D2H of Y every step)
+    xh = torch.from_numpy(x_host.view(np.int16)).view(torch.bfloat16).pin_memory()
+    yh = torch.empty((M, N), dtype=torch.bfloat16).pin_memory()
+    for i in range(min(args.warmup, 20)):
+        x.copy_(xh, non_blocking=True)
+        yy = step(i)
+        yh.copy_(yy, non_blocking=True)
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        x.copy_(xh, non_blocking=True)
+        yy = step(i)
+        yh.copy_(yy, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_val = flops_step * args.steps / (e2e_ms / 1e3) / 1e12
+
+    extras = {}
+    if not args.no_extras and world == 1:
+        extras = context_timings(Z, zh, w, layer, K, N, dev, R, l2)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample(layer, M, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": metric_name(), "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{layer} ZipGEMM M={M} (K={K}, N={N})", "layer": layer, "M": M, "K": K,
+                       "N": N, "weights": "N(0,0.02^2) fp32 -> bf16 RNE, TCA-TBE", "parallelism": f"cols{world}",
+                       "l2_hygiene": f"{R} rotated weight copies ({R * wbytes / 1e6:.0f} MB > 3x L2 {l2 / 1e6:.0f} MB)",
+                       "bits_per_element": zh_full.bits_per_element(), "base_exp": zh_full.base_exp,
+                       "coverage": zh_full.covered / (N * K), "graphs": graphs is not None},
+            "hbm_gbs": hbm_gbs,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                         "kernel": "zipgemm_kernel", "bytes_per_launch": bytes_launch,
+                         "kernel_us": kern_ms * 1e3},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": 2 * M * K,
+                    "d2h_bytes_per_step": 2 * M * N},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(),
+        }
+        if extras:
+            line["context"] = extras
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def context_timings(Z, zh, w, layer, K, N, dev, R, l2):
+    """cuBLAS BF16 (torch F.linear on the uncompressed W) vs ZipGEMM at M = 1, 8, 32 (context)."""
+    import torch
+    wd_dense = torch.from_numpy(w.view(np.int16)).view(torch.bfloat16).to(dev)
+    Rd = max(2, math.ceil(3 * l2 / (w.size * 2)))
+    dense = [wd_dense.clone() for _ in range(Rd)]
+    comp = [zh.to(dev) for _ in range(R)]
+    out = {}
+    for M in (1, 8, 32):
+        x = torch.randn((M, K), device=dev).to(torch.bfloat16)
+        ws = Z.workspace(M, N, K, dev)
+        y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+        res = {}
+        for name, fn, n in (("zipgemm", lambda i: Z.gemm(x, comp[i % R], out=y, ws=ws), R),
+                            ("cublas", lambda i: torch.mm(x, dense[i % Rd].t(), out=y), Rd)):
+            for i in range(10):
+                fn(i)
+            gs = []
+            s = torch.cuda.Stream(dev)
+            s.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(s):
+                fn(0)
+            torch.cuda.current_stream(dev).wait_stream(s)
+            for i in range(n):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    fn(i)
+                gs.append(g)
+            iters = 300
+            for i in range(20):
+                gs[i % n].replay()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            for i in range(iters):
+                gs[i % n].replay()
+            b.record()
+            torch.cuda.synchronize()
+            res[name + "_us"] = a.elapsed_time(b) * 1e3 / iters
+        res["speedup_vs_cublas"] = res["cublas_us"] / res["zipgemm_us"]
+        res["zipgemm_tflops"] = 2 * M * N * K / (res["zipgemm_us"] * 1e-6) / 1e12
+        res["zipgemm_gbs"] = (zh.nbytes() + 2 * M * K + 2 * M * N) / (res["zipgemm_us"] * 1e-6) / 1e9
+        out[f"M{M}"] = res
+    return out
+
+
+if __name__ == "__main__":
+    main()

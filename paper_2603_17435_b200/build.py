@@ -42,7 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if s.endswith(".cu"):
             cmd = [NVCC, *ARCH, *COMMON, "-Xptxas", "-v" if verbose else "-O3", "-c", s, "-o", o]
         else:
-            cmd = [NVCC, *COMMON, "-x", "c++", "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *COMMON, "-x", "c++", "-c", s, "-o", o]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)

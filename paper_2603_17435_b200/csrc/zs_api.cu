@@ -176,11 +176,22 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
   // X tensor map: dims {K, M}, row stride ldx*2 bytes, box {64, n_umma}, SWIZZLE_128B;
   // out-of-bounds rows/columns are zero-filled by the TMA unit.
   const int ngroups = zs::gemm_groups();
+  const size_t budget = 227 * 1024;
+  // token chunk: the largest of 256/128/64/32/16 whose A/X slots plus a compressed ring of
+  // kGroups slots fit in shared memory (each chunk re-decodes W; see DESIGN.md large-M)
+  int64_t chunk = 256;
+  for (; chunk >= 16; chunk /= 2) {
+    const int64_t nu = up(std::min<int64_t>(chunk, M), 16);
+    const size_t aslot = (size_t)up(16384 + nu * 128, 1024);
+    const size_t fixed = 1024 + 4096 + 1024 + (size_t)zs::gemm_aslots() * aslot;
+    if (fixed + (size_t)ngroups * p.cslot_bytes <= budget) break;
+  }
+  if (chunk < 16) return ZS_ERR_UNSUPPORTED;
   int launches = 0;
   CUtensorMap xmap;
   uint32_t cur_box = 0;
-  for (int64_t m0 = 0; m0 < M; m0 += 256) {
-    const int64_t mc = std::min<int64_t>(256, M - m0);
+  for (int64_t m0 = 0; m0 < M; m0 += chunk) {
+    const int64_t mc = std::min<int64_t>(chunk, M - m0);
     p.m0 = (int32_t)m0;
     p.mc = (int32_t)mc;
     p.n_umma = (uint32_t)up(mc, 16);
@@ -188,10 +199,7 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
     while (tc < 2 * p.n_umma) tc <<= 1;
     p.tmem_cols = tc;
     p.aslot_bytes = (uint32_t)up(16384 + (int64_t)p.n_umma * 128, 1024);
-    // compressed ring: largest multiple of the group count that fits in the smem budget
-    const size_t budget = 227 * 1024;
     const size_t fixed = 1024 + 4096 + 1024 + (size_t)zs::gemm_aslots() * p.aslot_bytes;
-    if (fixed + (size_t)ngroups * p.cslot_bytes > budget) return ZS_ERR_UNSUPPORTED;
     uint32_t ns = (uint32_t)((budget - fixed) / p.cslot_bytes);
     ns = std::min<uint32_t>(ns, 16);
     ns -= ns % ngroups;
