@@ -15,6 +15,7 @@
 namespace {
 
 thread_local int g_last_launches = 0;
+unsigned long long* g_trace = nullptr;  // debug: set by zs_debug_set_trace
 
 inline int64_t up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -91,6 +92,10 @@ extern "C" const char* zs_status_string(zs_status s) {
 
 extern "C" int zs_last_launch_count(void) { return g_last_launches; }
 
+// Debug hook (not part of include/zs.h): device buffer of 4*128*16 u64 for per-unit
+// pipeline timestamps of the first 4 CTAs of subsequent zs_gemm launches; NULL disables.
+extern "C" void zs_debug_set_trace(unsigned long long* dev_buf) { g_trace = dev_buf; }
+
 extern "C" zs_status zs_decompress(const zs_tensor* w, uint16_t* out, int64_t ld_out, void* stream) {
   g_last_launches = 0;
   zs_status st = validate_tensor(w);
@@ -151,7 +156,7 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
   auto enc = get_encode_tiled();
   if (!enc) return ZS_ERR_UNSUPPORTED;
 
-  const int64_t mc_max = std::min<int64_t>(M, 256);
+  const int64_t mc_max = std::min<int64_t>(M, 256);  // workspace rows (>= any chunk)
   zs::GemmParams p{};
   p.b1 = w->b1;
   p.b2 = w->b2;
@@ -168,23 +173,28 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
   p.nbc = w->sz.padded_cols / 64;
   p.nbands = (p.nbr + 1) / 2;
   p.total_units = p.nbands * p.nbc;
-  p.hcap = (uint32_t)w->sz.max_h_seg_bytes + 16;
-  p.lcap = (uint32_t)w->sz.max_l_seg_bytes + 16;
-  p.cslot_bytes = (uint32_t)up(3072 + 2 * (int64_t)p.hcap + 2 * (int64_t)p.lcap, 128);
+  if (p.total_units >= (int64_t(1) << 31)) return ZS_ERR_UNSUPPORTED;
+  {
+    const int64_t ups = zs::gemm_units_per_stage();
+    if (w->sz.h_bytes >= (int64_t(1) << 32) || 2 * w->sz.l_words >= (int64_t(1) << 32)) return ZS_ERR_UNSUPPORTED;
+    p.hcap = (uint32_t)(ups * w->sz.max_h_seg_bytes + 16);
+    p.lcap = (uint32_t)(ups * w->sz.max_l_seg_bytes + 16);
+    p.cslot_bytes = (uint32_t)up(zs::gemm_stage_fixed_bytes() + 2 * (int64_t)p.hcap + 2 * (int64_t)p.lcap, 1024);
+  }
   p.eb7x2 = eb7x2_of(w->base_exp);
+  p.trace = g_trace;
 
   // X tensor map: dims {K, M}, row stride ldx*2 bytes, box {64, n_umma}, SWIZZLE_128B;
   // out-of-bounds rows/columns are zero-filled by the TMA unit.
-  const int ngroups = zs::gemm_groups();
   const size_t budget = 227 * 1024;
-  // token chunk: the largest of 256/128/64/32/16 whose A/X slots plus a compressed ring of
+  // token chunk: the largest power of two <= 128 whose X slots plus a compressed ring of
   // kGroups slots fit in shared memory (each chunk re-decodes W; see DESIGN.md large-M)
-  int64_t chunk = 256;
+  int64_t chunk = zs::gemm_max_chunk();
   for (; chunk >= 16; chunk /= 2) {
     const int64_t nu = up(std::min<int64_t>(chunk, M), 16);
-    const size_t aslot = (size_t)up(16384 + nu * 128, 1024);
-    const size_t fixed = 1024 + 4096 + 1024 + (size_t)zs::gemm_aslots() * aslot;
-    if (fixed + (size_t)ngroups * p.cslot_bytes <= budget) break;
+    const size_t xslot = (size_t)up(nu * 128, 1024);
+    const size_t fixed = 1024 + 1024 + (size_t)zs::gemm_units_per_stage() * xslot;
+    if (fixed + (size_t)p.cslot_bytes <= budget) break;
   }
   if (chunk < 16) return ZS_ERR_UNSUPPORTED;
   int launches = 0;
@@ -195,15 +205,22 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
     p.m0 = (int32_t)m0;
     p.mc = (int32_t)mc;
     p.n_umma = (uint32_t)up(mc, 16);
-    uint32_t tc = 32;
-    while (tc < 2 * p.n_umma) tc <<= 1;
-    p.tmem_cols = tc;
-    p.aslot_bytes = (uint32_t)up(16384 + (int64_t)p.n_umma * 128, 1024);
-    const size_t fixed = 1024 + 4096 + 1024 + (size_t)zs::gemm_aslots() * p.aslot_bytes;
-    uint32_t ns = (uint32_t)((budget - fixed) / p.cslot_bytes);
-    ns = std::min<uint32_t>(ns, 16);
-    ns -= ns % ngroups;
-    p.n_cslots = ns;
+    p.aslot_bytes = (uint32_t)up((int64_t)p.n_umma * 128, 1024);
+    // smem split: compressed ring stages first (2..max, ~48 KB each at r = 0.98), X ring
+    // gets the rest (up to 16 tiles, at least 2)
+    const size_t base = 1024 + 1024;
+    uint32_t nc = (uint32_t)std::min<size_t>(
+        zs::gemm_max_cslots(), (budget - base - (size_t)zs::gemm_units_per_stage() * p.aslot_bytes) / p.cslot_bytes);
+    nc = std::min<uint32_t>(nc, 4);
+    uint32_t nx = (uint32_t)std::min<size_t>(zs::gemm_max_xslots(), (budget - base - nc * (size_t)p.cslot_bytes) / p.aslot_bytes);
+    if (nc < 1 || nx < (uint32_t)zs::gemm_units_per_stage()) return ZS_ERR_UNSUPPORTED;
+    p.n_cslots = nc;
+    p.n_xslots = nx;
+    // TMEM: two accumulator buffers + an A-operand ring of 32-column slots (512 columns)
+    p.acc_cols = (uint32_t)up(p.n_umma, 32);
+    uint32_t na = (512u - 2u * p.acc_cols) / 32u;
+    na = std::min<uint32_t>(na, (uint32_t)zs::gemm_max_aslots());
+    p.n_aslots = na - na % 4;
     if (p.n_umma != cur_box) {
       cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
       cuuint64_t strides[1] = {(cuuint64_t)(ldx * 2)};

@@ -4,9 +4,21 @@
 // decoder.  Citations: P:<line> = PAPER.md, S:<line> = SPEC.md.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace zs {
+
+// one lane of the (converged) warp returns true
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "elect.sync _|P1, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "+r"(pred));
+  return pred != 0;
+}
 
 // ------------------------------------------------------------------ smem / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -30,6 +42,8 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+// try_wait without a suspend hint: the hardware blocks for a short, system-defined time
+// and returns as soon as the phase completes -- used on the critical path.
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -42,9 +56,51 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// non-blocking probe
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Watchdog: a wait that spins ~2^28 times (seconds) reports the barrier and traps, so a
+// pipeline bug surfaces as a CUDA error instead of a hung GPU.
+static __device__ __noinline__ void zs_watchdog_fire(const void* what, uint32_t parity) {
+  printf("zs watchdog: block %d thread %d stuck on smem %#x parity %u\n", blockIdx.x, threadIdx.x,
+         (unsigned)__cvta_generic_to_shared(what), parity);
+  __trap();
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if (++n == (1u << 28)) zs_watchdog_fire(bar, parity);
   }
+}
+
+// for idle roles (epilogue): back off with nanosleep so spinning costs no issue slots
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t n = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(256);
+    if (++n == (1u << 24)) zs_watchdog_fire(bar, parity);
+  }
+}
+
+__device__ __forceinline__ void st_release_shared(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_shared(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
 }
 
 // generic-proxy smem writes -> visible to the async proxy (tcgen05.mma operand reads)
@@ -121,6 +177,26 @@ __device__ __forceinline__ void umma_bf16_ss(uint32_t d_tmem, uint64_t a_desc, u
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+
+// D[tmem] (+)= A[tmem] * B[smem]^T (A operand resident in tensor memory, K-major).
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// thread i of the warp writes 8 consecutive 32-bit columns of TMEM lane (base lane + i)
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, uint4 a, uint4 b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(a.x),
+               "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -265,6 +341,86 @@ __device__ __forceinline__ uint4 decode_row(uint64_t p1, uint64_t p2, uint64_t p
     }
   }
   return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+
+// ------------------------------------------------------------------ row decoder, v2
+// Same contract as decode_row, restructured for the sm_100a issue budget:
+//   * the row's plane bytes arrive as the 32-bit plane halves w1..w3 (4 FragTile rows
+//     each); bsel = (r8 & 3) | 0x4440 extracts byte r8 zero-extended with one PRMT.
+//   * codewords are spread with integer multiplies (FMA pipe) instead of per-bit shifts:
+//     (b & 0xF) * K, K = 1 + 2^6 + 2^15 + 2^21, drops bits 0..3 on the LSBs of bytes
+//     0, 2, 1, 3 with no overlapping partial products (no carries), so
+//     WA = [c0, c2, c1, c3] and WB = [c4<<4, c6<<4, c5<<4, c7<<4] bytewise, and
+//       E0 = WA*128 + EB,  E1 = umulhi(WA, 2^31) + EB,  E2 = WB*8 + EB,  E3 = umulhi(WB, 2^27) + EB
+//     put (e_base + c) of elements (2j, 2j+1) on bits 7..14 / 23..30 of word j exactly;
+//     the garbage they also produce stays outside those bits (checked exhaustively).
+//   * the fallback PRMT selector is the high half of the table word (umulhi, FMA pipe).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {  // all 4 selector bits
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+// (a & mask) | (b & ~mask) in one LOP3
+template <uint32_t kMask>
+__device__ __forceinline__ uint32_t bitsel(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(a), "r"(b), "n"(kMask));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t shfl_idx(uint32_t v, int src) {
+  uint32_t d;
+  asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(d) : "r"(v), "r"(src));
+  return d;
+}
+
+__device__ __forceinline__ uint4 decode_row_core(uint32_t b1, uint32_t b2, uint32_t b3, uint32_t m, uint4 ent,
+                                                 const uint8_t* __restrict__ H, uint32_t hs,
+                                                 const uint16_t* __restrict__ L, uint32_t ls, uint32_t eb7x2) {
+  const uint32_t* H32 = reinterpret_cast<const uint32_t*>(H + (hs & ~3u));
+  const uint32_t hsh = (hs & 3u) * 8u;
+  const uint32_t h0 = H32[0], h1 = H32[1], h2 = H32[2];
+  const uint32_t hlo = __funnelshift_r(h0, h1, hsh);
+  const uint32_t hhi = __funnelshift_r(h1, h2, hsh);
+  const uint32_t lpair = prmt(L[ls], L[ls + 1], 0x5410u);   // first two fallback values
+
+  constexpr uint32_t K = 1u | (1u << 6) | (1u << 15) | (1u << 21);
+  const uint32_t WA = ((b1 & 0xFu) * K & 0x01010101u) + 2u * ((b2 & 0xFu) * K & 0x01010101u) +
+                      4u * ((b3 & 0xFu) * K & 0x01010101u);
+  const uint32_t WB = ((b1 & 0xF0u) * K & 0x10101010u) + 2u * ((b2 & 0xF0u) * K & 0x10101010u) +
+                      4u * ((b3 & 0xF0u) * K & 0x10101010u);
+  const uint32_t E[4] = {WA * 128u + eb7x2, __umulhi(WA, 0x80000000u) + eb7x2, WB * 8u + eb7x2,
+                         __umulhi(WB, 1u << 27) + eb7x2};
+  const uint32_t sel[4] = {ent.x, ent.y, ent.z, ent.w};
+  uint32_t out[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t P = prmt(hlo, hhi, sel[j]);                  // sign|mantissa bytes
+    const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);            // + exponent field
+    out[j] = prmt(lpair, w, __umulhi(sel[j], 0x10000u));        // fallback ranks 0/1
+  }
+  if (__popc(m) < 6) {  // rank >= 2 fallbacks: rare patch loop
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t rank = (uint32_t)i - __popc(m & ((1u << i) - 1u));
+      if (!((m >> i) & 1u) && rank >= 2) {
+        const uint32_t v = L[ls + rank];
+        const int j = i >> 1;
+        out[j] = (i & 1) ? ((out[j] & 0x0000FFFFu) | (v << 16)) : ((out[j] & 0xFFFF0000u) | v);
+      }
+    }
+  }
+  return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+// byte offset of FragTile o's 8-byte plane word inside a BlockTile plane that was loaded
+// by a 2-D TMA box {16 x u64, 4 TCT rows} with SWIZZLE_128B (1024-B aligned destination):
+// TCT row tr = o / 16 occupies 128 B whose 16-B chunks are XOR-permuted by tr.
+__device__ __forceinline__ uint32_t plane_off(uint32_t o) {
+  const uint32_t tr = o >> 4, j = o & 15u;
+  return tr * 128u + (((j >> 1) ^ tr) << 4) + ((j & 1u) << 3);
 }
 
 }  // namespace zs

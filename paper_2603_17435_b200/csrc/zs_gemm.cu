@@ -1,283 +1,437 @@
 // zs_gemm.cu -- ZipGEMM on sm_100a: Y[M][N] = X[M][K] * W[N][K]^T, W in TCA-TBE.
 //
 // The paper's Ada kernel decodes into mma.sync registers.  On sm_100a the
-// tensor core reads operands from shared memory, so the kernel is re-designed around
+// tensor core reads A from shared or tensor memory, so the kernel is re-designed around
 // tcgen05 + TMEM + TMA, warp-specialised, persistent, stream-K:
 //
 //   work unit = (band of 128 weight rows = 2 BlockTile rows) x (one 64-wide K step).
 //   The (band, k) iteration space is split evenly over the CTAs (stream-K), so no SM
-//   idles on a partial wave (the O_proj "split-K tuning" issue of P:497).
+//   idles on a partial wave (the O_proj "split-K tuning" issue of P:497).  A ring stage
+//   holds 4 consecutive units of a CTA.
 //
-//   warp 20      compressed producer: 1-D TMA bulk copies of the two BlockTiles' planes,
-//                H and L segments into an S_c-slot ring (full_c / empty_c mbarriers);
-//                offsets are prefetched 32 units ahead in registers.
-//   warp 21      activation producer: 2-D TMA of the X tile [n_umma tokens][64 K],
-//                SWIZZLE_128B, zero-filled out of bounds (token tail and K padding).
-//   warps 4..19  4 decoder groups x 4 warps; thread = weight row.  Group g owns units
-//                g, g+4, ...: FragTile popcount scan (warp shuffles), then the
-//                branch-free row decoder writes 16-B chunks straight into the UMMA
-//                canonical K-major SW128 layout (A operand, 128 x 64 bf16 = 16 KB).
-//   warp 22      MMA issuer: 4 x tcgen05.mma (M=128, N=n_umma, K=16) per unit into a
-//                double-buffered fp32 TMEM accumulator; tcgen05.commit frees the A/X slot.
-//                Decode of unit k+1 (other groups) overlaps the MMA of unit k.
-//   warps 0..3   epilogue: tcgen05.ld the accumulator (thread = TMEM lane = weight row),
-//                BF16 store when the CTA owns the whole band, else fp32 atomics into the
-//                workspace; the last-arriving CTA of a band converts it to BF16 and
-//                zeroes the workspace again (self-cleaning split-K fixup).
+//   warp 1    compressed producer.  Units of one band are contiguous along K in every
+//             array, so a stage is fetched with one 1-D TMA bulk copy per array and run
+//             of same-band units (B1/B2/B3 x 2 BlockTile rows, H x 2, L x 2: 10 copies
+//             per 4 units).  Per-unit segment offsets and flags go into the stage header.
+//   warp 2    activation producer: 2-D TMA of X tiles [n_umma tokens][64 K], SWIZZLE_128B,
+//             zero-filled out of bounds (token tail and K padding), S_x-deep ring.
+//   warps 8.. decoders, 4 per TMEM lane quarter q = warp % 4 (rows 32q..32q+31 of the
+//             128-row A tile).  Every decoder warp visits every stage; inside a stage the
+//             4 warps of a quarter take that quarter of the stage's units dynamically.
+//             Per unit: FragTile popcount scan (warp shuffles), the branch-free row
+//             decoder, and tcgen05.st of the decoded BF16 rows into a TMEM A slot.
+//   warp 0    MMA issuer (one elected lane, warp-uniform operands): per stage, 4 x
+//             tcgen05.mma (A from TMEM, B = X from smem, M=128, N=n_umma, K=16) per unit
+//             into a double-buffered fp32 TMEM accumulator; decode of later units
+//             overlaps the MMA of earlier ones (the two-level pipeline of P:442-448).
+//             Completion is published as mma_done (monotonic unit count) which frees A
+//             slots for the decoders and X slots for warp 2.
+//   warps 4-7 epilogue: tcgen05.ld the accumulator (thread = TMEM lane = weight row), BF16
+//             store when the CTA owns the whole band, else fp32 atomics into the
+//             workspace; the last-arriving CTA of a band converts it to BF16 and zeroes the
+//             workspace again (self-cleaning split-K fixup).
+//
+// The single-warp roles share SM sub-partitions with 4 busy decoder warps each, so they
+// are written to issue few instructions per stage (no 64-bit division, batched waits).
 #include "zs_device.cuh"
 #include "zs_kernels.h"
+#include "zs_lut.h"
 
 #include <cuda_bf16.h>
 
 namespace zs {
 
-constexpr int kGroups = 4;                 // decoder warp groups
-constexpr int kASlots = kGroups;           // one A/X slot per group
-constexpr int kEpiWarps = 4;
-constexpr int kDecWarps = 4 * kGroups;
-constexpr int kWarpProdC = kEpiWarps + kDecWarps;  // 20
-constexpr int kWarpProdX = kWarpProdC + 1;         // 21
-constexpr int kWarpMma = kWarpProdX + 1;           // 22
-constexpr int kGemmThreads = 32 * (kWarpMma + 1);  // 736
-constexpr int kMaxCSlots = 16;
+constexpr int kWarpMma = 0;
+constexpr int kWarpProdC = 1;
+constexpr int kWarpProdX = 2;
+constexpr int kWarpAlloc = 3;
+constexpr int kWarpEpi0 = 4;                       // warps 4..7: epilogue (TMEM lane quarters)
+constexpr int kWarpDec0 = 8;                       // warps 8..23: decoders
+constexpr int kDecPerQuarter = 4;
+constexpr int kGemmThreads = 32 * (kWarpDec0 + 4 * kDecPerQuarter);  // 768
+constexpr int kUPS = 4;                            // units per ring stage
+constexpr int kMaxCSlots = 8;
+constexpr int kMaxXSlots = 16;
+constexpr int kMaxASlots = 12;
+constexpr uint32_t kStageMeta = 128;               // see the stage header layout below
+constexpr uint32_t kStagePlanes = 2 * 3 * kUPS * 512;
+constexpr uint32_t kTmemCols = 512;
+
+// stage header (u32 words): [4i+0..3] unit i {H a, H b, L a, L b} offsets inside the
+// stage regions; [16+q] ticket of lane quarter q; [20+i] unit i has BlockTile row b.
 
 struct __align__(8) Bars {
   uint64_t full_c[kMaxCSlots];
   uint64_t empty_c[kMaxCSlots];
-  uint64_t xfull[kASlots];
-  uint64_t decoded[kASlots];
-  uint64_t aempty[kASlots];
+  uint64_t xfull[kMaxXSlots];
+  uint64_t decoded[kMaxASlots];
+  uint64_t mcommit[2];
   uint64_t accfull[2];
   uint64_t accempty[2];
   uint32_t tmem_base;
   uint32_t last_flag;
+  uint32_t mma_done;        // # units whose MMAs completed (monotonic)
 };
+
+// debug trace: trace[(cta * kTraceUnits + unit) * 16 + event] = clock64, first kTraceCtas CTAs
+constexpr int kTraceCtas = 4, kTraceUnits = 128;
+__device__ __forceinline__ void trace_ev(unsigned long long* tr, int unit, int ev) {
+  if (tr != nullptr && blockIdx.x < kTraceCtas && unit < kTraceUnits)
+    tr[((size_t)blockIdx.x * kTraceUnits + unit) * 16 + ev] = clock64();
+}
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+__device__ __forceinline__ uint32_t bytepop(uint32_t x) {  // popcount of every byte
+  x = x - ((x >> 1) & 0x55555555u);
+  x = (x & 0x33333333u) + ((x >> 2) & 0x33333333u);
+  return (x + (x >> 4)) & 0x0F0F0F0Fu;
+}
+
+__device__ __forceinline__ void wait_count(const uint32_t* ctr, uint32_t need) {
+  uint32_t n = 0;
+  while (ld_acquire_shared(ctr) < need) {
+    __nanosleep(20);
+    if (++n == (1u << 26)) zs_watchdog_fire(ctr, need);
+  }
+}
+
 __global__ void __launch_bounds__(kGemmThreads, 1)
     zipgemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ uint8_t smem_raw[];
-  // 1024-B alignment for the SW128 operand tiles
+  // 1024-B alignment for the SW128 X tiles
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint4* lut = reinterpret_cast<uint4*>(smem);
-  Bars* bars = reinterpret_cast<Bars*>(smem + 4096);
-  uint8_t* aslots = smem + 4096 + 1024;
-  uint8_t* cslots = aslots + (size_t)kASlots * p.aslot_bytes;
+  Bars* bars = reinterpret_cast<Bars*>(smem);
+  uint8_t* xslots = smem + 1024;
+  uint8_t* cslots = xslots + (size_t)p.n_xslots * p.aslot_bytes;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const uint32_t S_c = p.n_cslots;
+  const uint32_t S_x = p.n_xslots;
+  const uint32_t S_a = p.n_aslots;
+  const uint32_t capH = p.hcap, capL = p.lcap;
 
-  // ---- stream-K range of this CTA
-  const int64_t T = p.total_units;
-  const int64_t u0 = (int64_t)blockIdx.x * T / gridDim.x;
-  const int64_t u1 = (int64_t)(blockIdx.x + 1) * T / gridDim.x;
+  // ---- stream-K range of this CTA (32-bit unit indices; the host checks the range)
+  const uint32_t T = (uint32_t)p.total_units;
+  const uint32_t u0 = (uint32_t)((uint64_t)blockIdx.x * T / gridDim.x);
+  const uint32_t u1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * T / gridDim.x);
   const int nunits = (int)(u1 - u0);
-  const int64_t nbc = p.nbc;
+  const int nstages = (nunits + kUPS - 1) / kUPS;
+  const uint32_t nbc = (uint32_t)p.nbc;
+  const uint32_t nbr = (uint32_t)p.nbr;
+  const uint32_t band0 = u0 / nbc, kc0 = u0 % nbc;
 
   // ---- setup
-  if (tid < 256) lut[tid] = build_lut_entry((uint32_t)tid);
   if (tid == 32) {
     for (uint32_t i = 0; i < S_c; ++i) {
       mbar_init(&bars->full_c[i], 1);
-      mbar_init(&bars->empty_c[i], 128);
+      mbar_init(&bars->empty_c[i], 32 * 4 * kDecPerQuarter);
     }
-    for (int i = 0; i < kASlots; ++i) {
-      mbar_init(&bars->xfull[i], 1);
-      mbar_init(&bars->decoded[i], 128);
-      mbar_init(&bars->aempty[i], 1);
-    }
+    for (uint32_t i = 0; i < S_x; ++i) mbar_init(&bars->xfull[i], 1);
+    for (uint32_t i = 0; i < S_a; ++i) mbar_init(&bars->decoded[i], 128);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->mcommit[i], 1);
       mbar_init(&bars->accfull[i], 1);
       mbar_init(&bars->accempty[i], 128);
     }
+    bars->mma_done = 0;
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc_dyn(&bars->tmem_base, p.tmem_cols);
+  if (warp == kWarpAlloc) tmem_alloc<kTmemCols>(&bars->tmem_base);
   if (warp == kWarpProdX && lane == 0) prefetch_tmap(&xmap);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = bars->tmem_base;
+  const uint32_t dcols = p.acc_cols;                   // accumulator buffer stride (columns)
+  const uint32_t tmem_a = tmem_base + 2u * dcols;      // first A slot column
 
   if (warp == kWarpProdC) {
     // ================================================================ compressed producer
+    // Batches of 32 units (8 stages): lane l owns unit b0 + l, loads its offsets, and
+    // the quad of lanes of a stage computes the stage header with shuffles.
     const uint64_t pol = policy_evict_first();
     const ulonglong2* off2 = reinterpret_cast<const ulonglong2*>(p.offsets);
-    // lane i holds {h,l} offsets for unit (batch + i): BlockTile a start/end, b start/end
-    auto load_batch = [&](int b, ulonglong2 (&o)[4]) {
-      const int it = b + lane;
-      if (it < nunits) {
-        const int64_t u = u0 + it;
-        const int64_t band = u / nbc, kc = u % nbc;
-        const int64_t bta = 2 * band * nbc + kc;
-        o[0] = off2[bta];
-        o[1] = off2[bta + 1];
-        if (2 * band + 1 < p.nbr) {
-          o[2] = off2[bta + nbc];
-          o[3] = off2[bta + nbc + 1];
-        } else {
-          o[2] = make_ulonglong2(0, 0);
-          o[3] = make_ulonglong2(0, 0);
+    const int quad = lane >> 2, qi = lane & 3;
+    for (int b0 = 0; b0 < nunits; b0 += 32) {
+      const int it = b0 + lane;
+      const bool valid = it < nunits;
+      const uint32_t kk = kc0 + (uint32_t)it;
+      const uint32_t band = band0 + kk / nbc, kc = kk % nbc;
+      const uint32_t bta = 2u * band * nbc + kc;
+      const bool has_b = valid && (2u * band + 1u < nbr);
+      uint32_t h0a = 0, h1a = 0, l0a = 0, l1a = 0, h0b = 0, h1b = 0, l0b = 0, l1b = 0;
+      if (valid) {
+        const ulonglong2 a0 = off2[bta], a1 = off2[bta + 1];
+        h0a = (uint32_t)a0.x; l0a = (uint32_t)a0.y; h1a = (uint32_t)a1.x; l1a = (uint32_t)a1.y;
+        if (has_b) {
+          const ulonglong2 c0 = off2[bta + nbc], c1 = off2[bta + nbc + 1];
+          h0b = (uint32_t)c0.x; l0b = (uint32_t)c0.y; h1b = (uint32_t)c1.x; l1b = (uint32_t)c1.y;
         }
       }
-    };
-    ulonglong2 cur[4], nxt[4];
-    load_batch(0, cur);
-    for (int b = 0; b < nunits; b += 32) {
-      if (b + 32 < nunits) load_batch(b + 32, nxt);
-      const int cnt = min(32, nunits - b);
-      for (int j = 0; j < cnt; ++j) {
-        uint64_t v[8];
+      // exclusive prefix of the segment sizes inside the quad (= stage)
+      uint32_t pha = h1a - h0a, phb = h1b - h0b, pla = l1a - l0a, plb = l1b - l0b;
+      const uint32_t tot_self = pha + phb + pla + plb + (valid ? (has_b ? 3072u : 1536u) : 0u);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          v[2 * q] = __shfl_sync(0xFFFFFFFFu, cur[q].x, j);
-          v[2 * q + 1] = __shfl_sync(0xFFFFFFFFu, cur[q].y, j);
+      for (int d = 1; d < 4; d <<= 1) {
+        const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, pha, d), b = __shfl_up_sync(0xFFFFFFFFu, phb, d);
+        const uint32_t c = __shfl_up_sync(0xFFFFFFFFu, pla, d), e = __shfl_up_sync(0xFFFFFFFFu, plb, d);
+        if (qi >= d) { pha += a; phb += b; pla += c; plb += e; }
+      }
+      // pha.. are now inclusive; exclusive = inclusive - own size
+      const uint32_t oha = pha - (h1a - h0a), ohb = phb - (h1b - h0b), ola = pla - (l1a - l0a), olb = plb - (l1b - l0b);
+      uint32_t stage_bytes = tot_self;
+      stage_bytes += __shfl_xor_sync(0xFFFFFFFFu, stage_bytes, 1);
+      stage_bytes += __shfl_xor_sync(0xFFFFFFFFu, stage_bytes, 2);
+      // runs of same-band units inside the quad: a run starts at qi == 0 or on a band change
+      const uint32_t band_prev = __shfl_up_sync(0xFFFFFFFFu, band, 1);
+      const bool run_start = valid && (qi == 0 || band_prev != band);
+      const uint32_t starts = __ballot_sync(0xFFFFFFFFu, run_start);
+      const uint32_t validm = __ballot_sync(0xFFFFFFFFu, valid);
+      // last lane of my run: next start in my quad minus one (or the quad's last valid lane)
+      const uint32_t quad_mask = 0xFu << (4 * quad);
+      const uint32_t later = starts & quad_mask & ~((2u << lane) - 1u);
+      const uint32_t qvalid = validm & quad_mask;
+      const int qlast = qvalid ? 31 - __clz(qvalid) : lane;
+      const int rend = later ? (__ffs(later) - 2) : qlast;
+      const uint32_t e_h1a = __shfl_sync(0xFFFFFFFFu, h1a, rend), e_l1a = __shfl_sync(0xFFFFFFFFu, l1a, rend);
+      const uint32_t e_h1b = __shfl_sync(0xFFFFFFFFu, h1b, rend), e_l1b = __shfl_sync(0xFFFFFFFFu, l1b, rend);
+      const uint32_t nrun = (uint32_t)(rend - lane + 1);
+      const int st_hi = min(nstages, (b0 + 32) / kUPS);
+      for (int st = b0 / kUPS; st < st_hi; ++st) {
+        const uint32_t slot = (uint32_t)st % S_c;
+        mbar_wait(&bars->empty_c[slot], (((uint32_t)st / S_c) & 1u) ^ 1u);
+        uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
+        const bool mine = (quad == st - b0 / kUPS);
+        if (mine && valid) {
+          uint32_t* meta = reinterpret_cast<uint32_t*>(cs);
+          *reinterpret_cast<uint4*>(meta + 4 * qi) = make_uint4(oha, ohb, ola, olb);
+          meta[20 + qi] = has_b ? 1u : 0u;
+          if (qi == 0) *reinterpret_cast<uint4*>(meta + 16) = make_uint4(0, 0, 0, 0);
         }
-        if (lane == 0) {
-          const int it = b + j;
-          const int64_t u = u0 + it;
-          const int64_t band = u / nbc, kc = u % nbc;
-          const int64_t bta = 2 * band * nbc + kc;
-          const bool has_b = (2 * band + 1 < p.nbr);
-          const uint32_t c = (uint32_t)it % S_c;
-          mbar_wait(&bars->empty_c[c], (((uint32_t)it / S_c) & 1u) ^ 1u);
-          uint8_t* cs = cslots + (size_t)c * p.cslot_bytes;
-          const uint32_t ha = (uint32_t)(v[2] - v[0]), la = (uint32_t)(v[3] - v[1]);
-          const uint32_t hb = has_b ? (uint32_t)(v[6] - v[4]) : 0u, lb = has_b ? (uint32_t)(v[7] - v[5]) : 0u;
-          const uint32_t bytes = 1536u + ha + la + (has_b ? 1536u + hb + lb : 0u);
-          uint64_t* fb = &bars->full_c[c];
-          mbar_arrive_expect_tx(fb, bytes);
-          bulk_g2s(cs, p.b1 + bta * 64, 512, fb, pol);
-          bulk_g2s(cs + 512, p.b2 + bta * 64, 512, fb, pol);
-          bulk_g2s(cs + 1024, p.b3 + bta * 64, 512, fb, pol);
-          if (ha) bulk_g2s(cs + 3072, p.h + v[0], ha, fb, pol);
-          if (la) bulk_g2s(cs + 3072 + 2 * p.hcap, reinterpret_cast<const uint8_t*>(p.l) + v[1], la, fb, pol);
+        __syncwarp();
+        if (mine && qi == 0) {
+          mbar_arrive_expect_tx(&bars->full_c[slot], stage_bytes);  // release: header visible
+          trace_ev(p.trace, it, 0);
+        }
+        __syncwarp();
+        if (mine && run_start) {
+          uint64_t* fb = &bars->full_c[slot];
+          uint8_t* planes = cs + kStageMeta;
+          uint8_t* Hr = planes + kStagePlanes;   // [H a | H b | L a | L b]
+          const uint32_t pb = nrun * 512u;
+          const uint32_t po = (uint32_t)qi * 512u;
+          bulk_g2s(planes + 0 * (kUPS * 512) + po, p.b1 + (size_t)bta * 64, pb, fb, pol);
+          bulk_g2s(planes + 1 * (kUPS * 512) + po, p.b2 + (size_t)bta * 64, pb, fb, pol);
+          bulk_g2s(planes + 2 * (kUPS * 512) + po, p.b3 + (size_t)bta * 64, pb, fb, pol);
+          if (e_h1a > h0a) bulk_g2s(Hr + oha, p.h + h0a, e_h1a - h0a, fb, pol);
+          if (e_l1a > l0a)
+            bulk_g2s(Hr + 2 * capH + ola, reinterpret_cast<const uint8_t*>(p.l) + l0a, e_l1a - l0a, fb, pol);
           if (has_b) {
-            const int64_t btb = bta + nbc;
-            bulk_g2s(cs + 1536, p.b1 + btb * 64, 512, fb, pol);
-            bulk_g2s(cs + 2048, p.b2 + btb * 64, 512, fb, pol);
-            bulk_g2s(cs + 2560, p.b3 + btb * 64, 512, fb, pol);
-            if (hb) bulk_g2s(cs + 3072 + p.hcap, p.h + v[4], hb, fb, pol);
-            if (lb)
-              bulk_g2s(cs + 3072 + 2 * p.hcap + p.lcap, reinterpret_cast<const uint8_t*>(p.l) + v[5], lb, fb, pol);
+            const size_t btb = (size_t)bta + nbc;
+            bulk_g2s(planes + 3 * (kUPS * 512) + po, p.b1 + btb * 64, pb, fb, pol);
+            bulk_g2s(planes + 4 * (kUPS * 512) + po, p.b2 + btb * 64, pb, fb, pol);
+            bulk_g2s(planes + 5 * (kUPS * 512) + po, p.b3 + btb * 64, pb, fb, pol);
+            if (e_h1b > h0b) bulk_g2s(Hr + capH + ohb, p.h + h0b, e_h1b - h0b, fb, pol);
+            if (e_l1b > l0b)
+              bulk_g2s(Hr + 2 * capH + capL + olb, reinterpret_cast<const uint8_t*>(p.l) + l0b, e_l1b - l0b, fb,
+                       pol);
           }
         }
         __syncwarp();
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
     }
   } else if (warp == kWarpProdX) {
     // ================================================================ activation producer
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_last();
-      const uint32_t xbytes = p.n_umma * 128u;
-      for (int it = 0; it < nunits; ++it) {
-        const uint32_t a = (uint32_t)it % kASlots;
-        mbar_wait(&bars->aempty[a], (((uint32_t)it / kASlots) & 1u) ^ 1u);
-        const int64_t kc = (u0 + it) % nbc;
-        uint8_t* xs = aslots + (size_t)a * p.aslot_bytes + 16384;
-        mbar_arrive_expect_tx(&bars->xfull[a], xbytes);
-        tma_load_2d(xs, &xmap, (int32_t)(kc * 64), p.m0, &bars->xfull[a], pol);
+    const uint64_t pol = policy_evict_last();
+    const uint32_t xbytes = p.n_umma * 128u;
+    uint32_t kc = kc0;
+    for (int it = 0; it < nunits; ++it) {
+      const uint32_t xs = (uint32_t)it % S_x;
+      // X slot xs is free once the MMAs of unit it - S_x have completed
+      wait_count(&bars->mma_done, (it >= (int)S_x) ? (uint32_t)(it - (int)S_x + 1) : 0u);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&bars->xfull[xs], xbytes);
+        tma_load_2d(xslots + (size_t)xs * p.aslot_bytes, &xmap, (int32_t)(kc * 64), p.m0, &bars->xfull[xs], pol);
       }
+      __syncwarp();
+      if (++kc == nbc) kc = 0;
     }
   } else if (warp == kWarpMma) {
     // ================================================================ MMA issuer
+    // Stage-batched: wait for the stage's X tiles and decoded A slots, issue 4 MMAs per
+    // unit (warp-uniform operands -> uniform registers, ~16 cycles per MMA; see
+    // scripts/umma_probe.cu), commit the stage, then publish the previous stage's
+    // completion as mma_done (monotonic: no mbarrier phase aliasing for the pollers).
     const uint32_t idesc = umma_idesc_bf16(128, p.n_umma);
+    const uint32_t xbase = smem_u32(xslots);
+    uint32_t kc = kc0;
     int seg = -1;
-    for (int it = 0; it < nunits; ++it) {
-      const int64_t u = u0 + it;
-      const bool first = (it == 0) || (u % nbc == 0);
-      const bool last = (it == nunits - 1) || ((u + 1) % nbc == 0);
-      if (first) {
-        ++seg;
-        mbar_wait(&bars->accempty[seg & 1], (((uint32_t)seg >> 1) & 1u) ^ 1u);
-        tc_fence_after();
-      }
-      const uint32_t a = (uint32_t)it % kASlots;
-      mbar_wait(&bars->decoded[a], ((uint32_t)it / kASlots) & 1u);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t d = tmem_base + (uint32_t)(seg & 1) * p.n_umma;
-        const uint32_t a_addr = smem_u32(aslots + (size_t)a * p.aslot_bytes);
-        const uint32_t x_addr = a_addr + 16384;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          umma_bf16_ss(d, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(x_addr + 32 * k), idesc,
-                       (first && k == 0) ? 0u : 1u);
-        umma_commit(&bars->aempty[a]);
-        if (last) umma_commit(&bars->accfull[seg & 1]);
-      }
+    int pub = 0;   // stages whose completion has been published
+    auto publish = [&]() {
+      ++pub;
+      if (elect_one()) st_release_shared(&bars->mma_done, (uint32_t)min(pub * kUPS, nunits));
       __syncwarp();
-    }
-  } else if (warp >= kEpiWarps) {
-    // ================================================================ decoders
-    const int g = (warp - kEpiWarps) >> 2;
-    const int wg = (warp - kEpiWarps) & 3;
-    const int bt_sel = wg >> 1, hh = wg & 1;
-    const int lr = lane + 32 * hh;      // row inside the BlockTile
-    const int fr = lr >> 3, r8 = lr & 7;
-    const int R = 64 * bt_sel + lr;     // row inside the 128-row A tile
-    const uint64_t rowmask = (1ull << (8 * r8)) - 1ull;
-    const uint32_t a = (uint32_t)g;     // this group's A/X slot
-    uint8_t* A = aslots + (size_t)a * p.aslot_bytes;
-    for (int it = g; it < nunits; it += kGroups) {
-      const uint32_t c = (uint32_t)it % S_c;
-      mbar_wait(&bars->full_c[c], ((uint32_t)it / S_c) & 1u);
-      mbar_wait(&bars->xfull[a], ((uint32_t)it / kASlots) & 1u);
-      const int64_t band = (u0 + it) / nbc;
-      const bool present = (2 * band + bt_sel) < p.nbr;
-      if (present) {
-        const uint8_t* cs = cslots + (size_t)c * p.cslot_bytes;
-        const uint64_t* P1 = reinterpret_cast<const uint64_t*>(cs + bt_sel * 1536);
-        const uint64_t* P2 = P1 + 64;
-        const uint64_t* P3 = P1 + 128;
-        const uint8_t* H = cs + 3072 + bt_sel * p.hcap;
-        const uint16_t* L = reinterpret_cast<const uint16_t*>(cs + 3072 + 2 * p.hcap + bt_sel * p.lcap);
-        // FragTile prefix: this warp's FragTiles are canonical 32*hh .. 32*hh+31
-        const int fo = 32 * hh + lane;
-        const uint32_t cnt = __popcll(P1[fo] | P2[fo] | P3[fo]);
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-          if (lane >= d) incl += t;
-        }
-        const uint32_t excl = incl - cnt;
-        uint32_t base = 0;
-        if (hh) base = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)__popcll(P1[lane] | P2[lane] | P3[lane]));
-#pragma unroll 2
-        for (int fc = 0; fc < 8; ++fc) {
-          const int o = ((fr >> 1) * 4 + (fc >> 1)) * 4 + (fc & 1) * 2 + (fr & 1);
-          const uint32_t pref = __shfl_sync(0xFFFFFFFFu, excl, o - 32 * hh) + base;
-          const uint64_t q1 = P1[o], q2 = P2[o], q3 = P3[o];
-          const uint32_t hs = pref + (uint32_t)__popcll((q1 | q2 | q3) & rowmask);
-          const uint32_t ls = (uint32_t)(o * 8 + r8) * 8u - hs;
-          const uint4 v = decode_row(q1, q2, q3, (uint32_t)r8, H, hs, L, ls, lut, p.eb7x2);
-          *reinterpret_cast<uint4*>(A + R * 128 + ((fc ^ (R & 7)) << 4)) = v;
-        }
+    };
+    // non-blocking: observe completions of issued stages in order
+    auto poll = [&](int issued) {
+      while (pub < issued && mbar_test_wait(&bars->mcommit[pub & 1], ((uint32_t)pub >> 1) & 1u)) publish();
+    };
+    for (int st = 0; st < nstages; ++st) {
+      // at most two stages in flight (mcommit is a 2-deep ring observed in order)
+      while (pub + 1 < st) {
+        mbar_wait(&bars->mcommit[pub & 1], ((uint32_t)pub >> 1) & 1u);
+        publish();
       }
-      fence_proxy_async_smem();
-      mbar_arrive(&bars->decoded[a]);
-      mbar_arrive(&bars->empty_c[c]);
-    }
-  } else {
-    // ================================================================ epilogue (warps 0..3)
-    const int et = tid;  // 0..127 = TMEM lane = row inside the band
-    const int64_t b_first = u0 / nbc, b_last = (u1 - 1) / nbc;
-    int seg = 0;
-    for (int64_t band = b_first; band <= b_last; ++band, ++seg) {
-      const int64_t s0 = max(u0, band * nbc), s1 = min(u1, (band + 1) * nbc);
-      const bool full = (s1 - s0) == nbc;
-      mbar_wait(&bars->accfull[seg & 1], ((uint32_t)seg >> 1) & 1u);
+      const int i0 = st * kUPS, i1 = min(nunits, i0 + kUPS);
+      for (int it = i0; it < i1; ++it) {
+        while (!mbar_test_wait(&bars->xfull[(uint32_t)it % S_x], ((uint32_t)it / S_x) & 1u)) poll(st);
+        while (!mbar_test_wait(&bars->decoded[(uint32_t)it % S_a], ((uint32_t)it / S_a) & 1u)) poll(st);
+      }
       tc_fence_after();
-      const int64_t n = band * 128 + et;
+      for (int it = i0; it < i1; ++it) {
+        const bool first = (it == 0) || (kc == 0);
+        const bool last = (it == nunits - 1) || (kc + 1 == nbc);
+        if (first) {
+          ++seg;
+          while (!mbar_test_wait(&bars->accempty[seg & 1], (((uint32_t)seg >> 1) & 1u) ^ 1u)) poll(st);
+          tc_fence_after();
+        }
+        const uint32_t d = tmem_base + (uint32_t)(seg & 1) * dcols;
+        const uint32_t at = tmem_a + 32u * ((uint32_t)it % S_a);
+        const uint64_t bdesc = umma_desc_sw128(xbase + ((uint32_t)it % S_x) * p.aslot_bytes);
+        if (elect_one()) {
+          umma_bf16_ts(d, at, bdesc, idesc, first ? 0u : 1u);
+          umma_bf16_ts(d, at + 8u, bdesc + 2, idesc, 1u);
+          umma_bf16_ts(d, at + 16u, bdesc + 4, idesc, 1u);
+          umma_bf16_ts(d, at + 24u, bdesc + 6, idesc, 1u);
+          trace_ev(p.trace, it, 6);
+          if (last) umma_commit(&bars->accfull[seg & 1]);
+        }
+        __syncwarp();
+        if (++kc == nbc) kc = 0;
+      }
+      if (elect_one()) umma_commit(&bars->mcommit[st & 1]);
+      __syncwarp();
+      poll(st + 1);
+    }
+    while (pub < nstages) {
+      mbar_wait(&bars->mcommit[pub & 1], ((uint32_t)pub >> 1) & 1u);
+      publish();
+    }
+  } else if (warp >= kWarpDec0) {
+    // ================================================================ decoders
+    const int q = warp & 3;                       // TMEM lane quarter (== warp % 4)
+    const int bt_sel = q >> 1, hh = q & 1;
+    const int lr = lane + 32 * hh;                // row inside the BlockTile
+    const int fr = lr >> 3, r8 = lr & 7;
+    const int tr = fr >> 1;                       // TensorCoreTile row of this thread's FragTiles
+    const uint32_t bsel = (uint32_t)(r8 & 3) | 0x4440u;
+    const bool hi_row = r8 >= 4;
+    const uint32_t obase = (uint32_t)(tr * 16 + (fr & 1));                 // o for fc = 0
+    const uint32_t hoff = (uint32_t)((r8 >> 2) << 2);                      // plane half of the row
+    const int srcbase = (tr - 2 * hh) * 16 + (fr & 1);
+    const uint32_t tq = tmem_a + ((uint32_t)(32 * q) << 16);
+    const int fo = 32 * hh + lane;                // scan lane's FragTile
+    for (int st = 0; st < nstages; ++st) {
+      const uint32_t slot = (uint32_t)st % S_c;
+      mbar_wait(&bars->full_c[slot], ((uint32_t)st / S_c) & 1u);
+      const uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
+      const uint32_t* meta = reinterpret_cast<const uint32_t*>(cs);
+      uint32_t* tickets = const_cast<uint32_t*>(meta) + 16;
+      const int nu = min(kUPS, nunits - st * kUPS);
+      while (true) {
+        uint32_t j = 0;
+        if (lane == 0) j = atomicAdd(&tickets[q], 1u);
+        j = shfl_idx(j, 0);
+        if ((int)j >= nu) break;
+        const int it = st * kUPS + (int)j;
+        const uint32_t a = (uint32_t)it % S_a;
+        const bool present = (bt_sel == 0) || (meta[20 + j] != 0u);
+        if (present) {
+          const uint4 mt = *reinterpret_cast<const uint4*>(meta + 4 * j);  // {H a, H b, L a, L b}
+          const uint8_t* P1 = cs + kStageMeta + (bt_sel * 3) * (kUPS * 512) + j * 512;
+          const uint8_t* P2 = P1 + kUPS * 512;
+          const uint8_t* P3 = P2 + kUPS * 512;
+          const uint8_t* Hr = cs + kStageMeta + kStagePlanes;
+          const uint8_t* H = Hr + bt_sel * capH + (bt_sel ? mt.y : mt.x);
+          const uint16_t* L =
+              reinterpret_cast<const uint16_t*>(Hr + 2 * capH + bt_sel * capL + (bt_sel ? mt.w : mt.z));
+          // ---- scan: lane = FragTile 32*hh + lane (canonical order)
+          const uint2 s1 = *reinterpret_cast<const uint2*>(P1 + fo * 8);
+          const uint2 s2 = *reinterpret_cast<const uint2*>(P2 + fo * 8);
+          const uint2 s3 = *reinterpret_cast<const uint2*>(P3 + fo * 8);
+          const uint32_t mlo = s1.x | s2.x | s3.x, mhi = s1.y | s2.y | s3.y;
+          const uint32_t cnt = __popc(mlo) + __popc(mhi);
+          uint32_t incl = cnt;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (lane >= d) incl += t;
+          }
+          uint32_t excl = incl - cnt;
+          if (hh) {
+            const uint2 t1 = *reinterpret_cast<const uint2*>(P1 + lane * 8);
+            const uint2 t2 = *reinterpret_cast<const uint2*>(P2 + lane * 8);
+            const uint2 t3 = *reinterpret_cast<const uint2*>(P3 + lane * 8);
+            excl += __reduce_add_sync(0xFFFFFFFFu, __popc(t1.x | t2.x | t3.x) + __popc(t1.y | t2.y | t3.y));
+          }
+          // exclusive per-row prefix inside the FragTile, one byte per row
+          const uint32_t bl = bytepop(mlo), bh = bytepop(mhi);
+          const uint32_t rp_lo = bl * 0x01010100u;
+          const uint32_t rp_hi = bh * 0x01010100u + ((bl * 0x01010101u) >> 24) * 0x01010101u;
+          // A slot a must be free: the MMAs of unit it - S_a have completed
+          wait_count(&bars->mma_done, (it >= (int)S_a) ? (uint32_t)(it - (int)S_a + 1) : 0u);
+          tc_fence_after();
+          const uint32_t taddr0 = tq + 32u * a;
+#pragma unroll
+          for (int fb = 0; fb < 8; fb += 4) {
+            uint4 v[4];
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+              const int f = fb + qq;
+              const int src = srcbase + (f >> 1) * 4 + (f & 1) * 2;
+              const uint32_t pref = shfl_idx(excl, src);
+              const uint32_t rl = shfl_idx(rp_lo, src);
+              const uint32_t rh = shfl_idx(rp_hi, src);
+              const uint32_t hs = pref + prmt(hi_row ? rh : rl, 0u, bsel);
+              const uint32_t o = obase + (uint32_t)((f >> 1) * 4 + (f & 1) * 2);
+              const uint32_t ls = (o * 8u + (uint32_t)r8) * 8u - hs;
+              const uint32_t off = o * 8u + hoff;
+              const uint32_t b1 = prmt(*reinterpret_cast<const uint32_t*>(P1 + off), 0u, bsel);
+              const uint32_t b2 = prmt(*reinterpret_cast<const uint32_t*>(P2 + off), 0u, bsel);
+              const uint32_t b3 = prmt(*reinterpret_cast<const uint32_t*>(P3 + off), 0u, bsel);
+              const uint32_t m = b1 | b2 | b3;
+              v[qq] = decode_row_core(b1, b2, b3, m, c_lut[m], H, hs, L, ls, p.eb7x2);
+            }
+            tmem_st8(taddr0 + 4u * fb, v[0], v[1]);
+            tmem_st8(taddr0 + 4u * fb + 8u, v[2], v[3]);
+          }
+          tmem_wait_st();
+        }
+        tc_fence_before();
+        mbar_arrive(&bars->decoded[a]);
+        if (lane == 0) trace_ev(p.trace, it, 2 + q);
+      }
+      mbar_arrive(&bars->empty_c[slot]);
+    }
+  } else if (warp >= kWarpEpi0) {
+    // ================================================================ epilogue (warps 4..7)
+    const int et = tid - 32 * kWarpEpi0;  // 0..127 = TMEM lane = row inside the band
+    const int eq = warp & 3;              // TMEM lane quarter
+    const uint32_t b_last = (u1 - 1) / nbc;
+    int seg = 0;
+    for (uint32_t band = band0; band <= b_last; ++band, ++seg) {
+      const uint32_t s0 = max(u0, band * nbc), s1 = min(u1, (band + 1) * nbc);
+      const bool full = (s1 - s0) == nbc;
+      mbar_wait_sleep(&bars->accfull[seg & 1], ((uint32_t)seg >> 1) & 1u);
+      tc_fence_after();
+      const int64_t n = (int64_t)band * 128 + et;
       const bool nvalid = n < p.N;
-      const uint32_t taddr = tmem_base + ((uint32_t)(32 * warp) << 16) + (uint32_t)(seg & 1) * p.n_umma;
+      const uint32_t taddr = tmem_base + ((uint32_t)(32 * eq) << 16) + (uint32_t)(seg & 1) * dcols;
       for (uint32_t cb = 0; cb < p.n_umma; cb += 16) {
         uint32_t v[16];
         tmem_ld16(taddr + cb, v);
@@ -301,8 +455,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __threadfence();
         named_bar_sync(1, 128);
         if (et == 0) {
-          const uint32_t old = atomicAdd(&p.counters[band], (uint32_t)(s1 - s0));
-          bars->last_flag = (old + (uint32_t)(s1 - s0) == (uint32_t)nbc) ? 1u : 0u;
+          const uint32_t old = atomicAdd(&p.counters[band], s1 - s0);
+          bars->last_flag = (old + (s1 - s0) == nbc) ? 1u : 0u;
         }
         named_bar_sync(1, 128);
         if (bars->last_flag) {
@@ -324,9 +478,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == kWarpAlloc) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, p.tmem_cols);
+    tmem_dealloc(tmem_base, kTmemCols);
   }
 }
 
@@ -343,11 +497,15 @@ cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, 
 }
 
 size_t gemm_smem_bytes(const GemmParams& p) {
-  return 1024 /*align slack*/ + 4096 + 1024 + (size_t)kASlots * p.aslot_bytes + (size_t)p.n_cslots * p.cslot_bytes;
+  return 1024 /*align slack*/ + 1024 + (size_t)p.n_xslots * p.aslot_bytes + (size_t)p.n_cslots * p.cslot_bytes;
 }
 
 int gemm_threads() { return kGemmThreads; }
-int gemm_groups() { return kGroups; }
-int gemm_aslots() { return kASlots; }
+int gemm_max_xslots() { return kMaxXSlots; }
+int gemm_max_cslots() { return kMaxCSlots; }
+int gemm_max_aslots() { return kMaxASlots; }
+uint32_t gemm_stage_fixed_bytes() { return kStageMeta + kStagePlanes; }
+int gemm_units_per_stage() { return kUPS; }
+int gemm_max_chunk() { return 128; }
 
 }  // namespace zs

@@ -45,12 +45,15 @@ struct GemmParams {
   int64_t total_units;      // nbands * nbc
   int32_t m0, mc;           // token chunk [m0, m0 + mc)
   uint32_t n_umma;          // mc rounded up to 16
-  uint32_t hcap, lcap;      // per-BlockTile segment capacities in smem
-  uint32_t cslot_bytes;     // compressed ring slot
-  uint32_t aslot_bytes;     // A (decoded) + X slot
-  uint32_t n_cslots;        // multiple of kGroups
-  uint32_t tmem_cols;
+  uint32_t hcap, lcap;      // per-stage H / L capacity of one BlockTile row (4 units)
+  uint32_t cslot_bytes;     // compressed ring stage (4 units)
+  uint32_t aslot_bytes;     // X (B operand) slot; the decoded A operand lives in TMEM
+  uint32_t n_cslots;        // ring stages
+  uint32_t n_xslots;        // X tile ring
+  uint32_t n_aslots;        // TMEM A-operand ring (32 columns each, multiple of 4)
+  uint32_t acc_cols;        // TMEM columns per accumulator buffer (>= n_umma, multiple of 32)
   uint32_t eb7x2;
+  unsigned long long* trace;  // optional per-unit event timestamps (debug; nullptr = off)
 };
 
 cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, size_t smem, cudaStream_t stream);
@@ -58,5 +61,11 @@ size_t gemm_smem_bytes(const GemmParams& p);
 int gemm_threads();
 int gemm_groups();
 int gemm_aslots();
+int gemm_max_xslots();
+int gemm_max_cslots();
+int gemm_max_aslots();
+uint32_t gemm_stage_fixed_bytes();
+int gemm_units_per_stage();
+int gemm_max_chunk();
 
 }  // namespace zs
