@@ -16,6 +16,7 @@ namespace {
 
 thread_local int g_last_launches = 0;
 unsigned long long* g_trace = nullptr;  // debug: set by zs_debug_set_trace
+uint32_t g_max_cslots = 3;              // ring depth cap (tunable via zs_debug_set_ring)
 
 inline int64_t up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -95,6 +96,7 @@ extern "C" int zs_last_launch_count(void) { return g_last_launches; }
 // Debug hook (not part of include/zs.h): device buffer of 4*128*16 u64 for per-unit
 // pipeline timestamps of the first 4 CTAs of subsequent zs_gemm launches; NULL disables.
 extern "C" void zs_debug_set_trace(unsigned long long* dev_buf) { g_trace = dev_buf; }
+extern "C" void zs_debug_set_ring(int max_cslots) { g_max_cslots = (uint32_t)std::max(1, max_cslots); }
 
 extern "C" zs_status zs_decompress(const zs_tensor* w, uint16_t* out, int64_t ld_out, void* stream) {
   g_last_launches = 0;
@@ -193,7 +195,7 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
   for (; chunk >= 16; chunk /= 2) {
     const int64_t nu = up(std::min<int64_t>(chunk, M), 16);
     const size_t xslot = (size_t)up(nu * 128, 1024);
-    const size_t fixed = 1024 + 1024 + (size_t)zs::gemm_units_per_stage() * xslot;
+    const size_t fixed = zs::gemm_fixed_smem() + (size_t)zs::gemm_units_per_stage() * xslot;
     if (fixed + (size_t)p.cslot_bytes <= budget) break;
   }
   if (chunk < 16) return ZS_ERR_UNSUPPORTED;
@@ -208,11 +210,12 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
     p.aslot_bytes = (uint32_t)up((int64_t)p.n_umma * 128, 1024);
     // smem split: compressed ring stages first (2..max, ~48 KB each at r = 0.98), X ring
     // gets the rest (up to 16 tiles, at least 2)
-    const size_t base = 1024 + 1024;
+    const size_t base = zs::gemm_fixed_smem();
     uint32_t nc = (uint32_t)std::min<size_t>(
         zs::gemm_max_cslots(), (budget - base - (size_t)zs::gemm_units_per_stage() * p.aslot_bytes) / p.cslot_bytes);
-    nc = std::min<uint32_t>(nc, 4);
+    nc = std::min<uint32_t>(nc, g_max_cslots);
     uint32_t nx = (uint32_t)std::min<size_t>(zs::gemm_max_xslots(), (budget - base - nc * (size_t)p.cslot_bytes) / p.aslot_bytes);
+    nx -= nx % (uint32_t)zs::gemm_units_per_stage();
     if (nc < 1 || nx < (uint32_t)zs::gemm_units_per_stage()) return ZS_ERR_UNSUPPORTED;
     p.n_cslots = nc;
     p.n_xslots = nx;

@@ -84,12 +84,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-// for idle roles (epilogue): back off with nanosleep so spinning costs no issue slots
+// for idle roles (epilogue): try_wait with a suspend-time hint -- the warp is descheduled
+// (no issue slots) until the phase completes or ~the hint elapses
+__device__ __forceinline__ bool mbar_try_wait_suspend(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   uint32_t n = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    __nanosleep(256);
-    if (++n == (1u << 24)) zs_watchdog_fire(bar, parity);
+  while (!mbar_try_wait_suspend(bar, parity, 1000000u)) {
+    if (++n == (1u << 20)) zs_watchdog_fire(bar, parity);
   }
 }
 
@@ -277,6 +289,10 @@ __device__ __forceinline__ uint4 build_lut_entry(uint32_t m) {
     }
     e[j] = hs | (fs << 16);
   }
+  // bit 7 (sign-replicate of the high-byte selector of element 0; copy and replicate give
+  // the same bit 15) flags rows with >= 3 fallbacks
+  e[0] &= ~0x80u;
+  if (__popc(m) < 6) e[0] |= 0x80u;
   return make_uint4(e[0], e[1], e[2], e[3]);
 }
 
@@ -376,43 +392,96 @@ __device__ __forceinline__ uint32_t shfl_idx(uint32_t v, int src) {
   return d;
 }
 
-__device__ __forceinline__ uint4 decode_row_core(uint32_t b1, uint32_t b2, uint32_t b3, uint32_t m, uint4 ent,
-                                                 const uint8_t* __restrict__ H, uint32_t hs,
-                                                 const uint16_t* __restrict__ L, uint32_t ls, uint32_t eb7x2) {
-  const uint32_t* H32 = reinterpret_cast<const uint32_t*>(H + (hs & ~3u));
-  const uint32_t hsh = (hs & 3u) * 8u;
-  const uint32_t h0 = H32[0], h1 = H32[1], h2 = H32[2];
-  const uint32_t hlo = __funnelshift_r(h0, h1, hsh);
-  const uint32_t hhi = __funnelshift_r(h1, h2, hsh);
-  const uint32_t lpair = prmt(L[ls], L[ls + 1], 0x5410u);   // first two fallback values
+// Multipliers of the row decoder, read from constant memory so that ptxas keeps the
+// multiply-adds on the FMA pipe (with immediates it strength-reduces them to LEA / SHF,
+// which issue on the ALU pipe -- the decoder's bottleneck).
+#define ZS_KSPREAD (1u | (1u << 6) | (1u << 15) | (1u << 21))
+__constant__ uint32_t c_mul[16] = {1u << 28, 128u, 1u << 31, 8u, 1u << 27, 1u << 16, 0xFFFFFFFEu, 0xFFFFFFFFu,
+                                   ZS_KSPREAD, ZS_KSPREAD << 1, ZS_KSPREAD << 2, ZS_KSPREAD << 4,
+                                   ZS_KSPREAD << 5, ZS_KSPREAD << 6, 0u, 0u};
+#ifndef ZS_CMUL
+#define ZS_CMUL 0
+#endif
+#if ZS_CMUL
+#define ZS_MUL(idx, imm) c_mul[idx]
+#else
+#define ZS_MUL(idx, imm) (imm)
+#endif
+enum : int { kM28 = 0, kM7 = 1, kM31 = 2, kM3 = 3, kM27 = 4, kM16 = 5, kMNeg2 = 6, kMNeg1 = 7, kMK = 8, kMK4 = 11 };
 
-  constexpr uint32_t K = 1u | (1u << 6) | (1u << 15) | (1u << 21);
-  const uint32_t WA = ((b1 & 0xFu) * K & 0x01010101u) + 2u * ((b2 & 0xFu) * K & 0x01010101u) +
-                      4u * ((b3 & 0xFu) * K & 0x01010101u);
-  const uint32_t WB = ((b1 & 0xF0u) * K & 0x10101010u) + 2u * ((b2 & 0xF0u) * K & 0x10101010u) +
-                      4u * ((b3 & 0xF0u) * K & 0x10101010u);
-  const uint32_t E[4] = {WA * 128u + eb7x2, __umulhi(WA, 0x80000000u) + eb7x2, WB * 8u + eb7x2,
-                         __umulhi(WB, 1u << 27) + eb7x2};
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {  // a*b + c (FMA pipe)
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {  // hi(a*b) + c (FMA pipe)
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// Spread the 8 codeword bits of one plane byte b (bit i = element i) for WA / WB:
+//   lo = (b & 0xF) * K  and  hi = (b & 0xF0) * K, computed on the FMA pipe without the
+//   nibble masks: h4 = b >> 4 (= umulhi(b, 2^28)), hi = h4 * (K << 4), lo = b*K - hi.
+// kShift scales the plane (codeword bit k -> x2^k) through K.
+template <int kShift>
+__device__ __forceinline__ void spread_plane(uint32_t b, uint32_t& lo, uint32_t& hi) {
+  const uint32_t h4 = mad_hi(b, ZS_MUL(kM28, 1u << 28), 0u);
+  hi = mad_lo(h4, ZS_MUL(kMK4 + kShift, ZS_KSPREAD << (4 + kShift)), 0u);
+  lo = mad_lo(b, ZS_MUL(kMK + kShift, ZS_KSPREAD << kShift), mad_lo(hi, ZS_MUL(kMNeg1, 0xFFFFFFFFu), 0u));
+}
+
+// Row decoder on absolute smem pointers (the GEMM precomputes them):
+//   H32 : 4-byte aligned word containing the row's first H byte, hsh8 = 8 * (that byte's
+//         offset) -- only its low 5 bits are used (funnel shift wraps mod 32)
+//   Lrow: the row's first fallback value
+// Rows with >= 3 fallbacks (rank >= 2) are flagged by bit 7 of ent.x (the sign-replicate
+// bit of a selector nibble whose two modes give the same result) and patched on a rare path.
+__device__ __forceinline__ uint4 decode_row_abs(uint32_t b1, uint32_t b2, uint32_t b3, uint32_t m, uint4 ent,
+                                                const uint32_t* __restrict__ H32, uint32_t hsh8,
+                                                const uint16_t* __restrict__ Lrow, uint32_t eb7x2) {
+  const uint32_t h0 = H32[0], h1 = H32[1], h2 = H32[2];
+  const uint32_t hlo = __funnelshift_r(h0, h1, hsh8);
+  const uint32_t hhi = __funnelshift_r(h1, h2, hsh8);
+  const uint32_t lpair = prmt(Lrow[0], Lrow[1], 0x5410u);   // first two fallback values
+
+  uint32_t l1, u1, l2, u2, l3, u3;
+  spread_plane<0>(b1, l1, u1);
+  spread_plane<1>(b2, l2, u2);
+  spread_plane<2>(b3, l3, u3);
+  // WA = [c0, c2, c1, c3], WB = [c4<<4, c6<<4, c5<<4, c7<<4] bytewise (see decode_row_w)
+  const uint32_t WA = (l1 & 0x01010101u) | (l2 & 0x02020202u) | (l3 & 0x04040404u);
+  const uint32_t WB = (u1 & 0x10101010u) | (u2 & 0x20202020u) | (u3 & 0x40404040u);
+  const uint32_t E[4] = {mad_lo(WA, ZS_MUL(kM7, 128u), eb7x2), mad_hi(WA, ZS_MUL(kM31, 1u << 31), eb7x2),
+                         mad_lo(WB, ZS_MUL(kM3, 8u), eb7x2), mad_hi(WB, ZS_MUL(kM27, 1u << 27), eb7x2)};
   const uint32_t sel[4] = {ent.x, ent.y, ent.z, ent.w};
   uint32_t out[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const uint32_t P = prmt(hlo, hhi, sel[j]);                  // sign|mantissa bytes
     const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);            // + exponent field
-    out[j] = prmt(lpair, w, __umulhi(sel[j], 0x10000u));        // fallback ranks 0/1
+    out[j] = prmt(lpair, w, mad_hi(sel[j], ZS_MUL(kM16, 1u << 16), 0u));      // fallback ranks 0/1
   }
-  if (__popc(m) < 6) {  // rank >= 2 fallbacks: rare patch loop
+  if (ent.x & 0x80u) {  // rank >= 2 fallbacks: rare patch loop
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t rank = (uint32_t)i - __popc(m & ((1u << i) - 1u));
       if (!((m >> i) & 1u) && rank >= 2) {
-        const uint32_t v = L[ls + rank];
+        const uint32_t v = Lrow[rank];
         const int j = i >> 1;
         out[j] = (i & 1) ? ((out[j] & 0x0000FFFFu) | (v << 16)) : ((out[j] & 0xFFFF0000u) | v);
       }
     }
   }
   return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+__device__ __forceinline__ uint4 decode_row_core(uint32_t b1, uint32_t b2, uint32_t b3, uint32_t m, uint4 ent,
+                                                 const uint8_t* __restrict__ H, uint32_t hs,
+                                                 const uint16_t* __restrict__ L, uint32_t ls, uint32_t eb7x2) {
+  return decode_row_abs(b1, b2, b3, m, ent, reinterpret_cast<const uint32_t*>(H + (hs & ~3u)), hs * 8u, L + ls,
+                        eb7x2);
 }
 
 // byte offset of FragTile o's 8-byte plane word inside a BlockTile plane that was loaded

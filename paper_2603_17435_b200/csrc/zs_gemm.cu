@@ -47,15 +47,21 @@ constexpr int kWarpProdX = 2;
 constexpr int kWarpAlloc = 3;
 constexpr int kWarpEpi0 = 4;                       // warps 4..7: epilogue (TMEM lane quarters)
 constexpr int kWarpDec0 = 8;                       // warps 8..23: decoders
-constexpr int kDecPerQuarter = 4;
-constexpr int kGemmThreads = 32 * (kWarpDec0 + 4 * kDecPerQuarter);  // 768
+constexpr int kDecPerQuarter = 6;
+constexpr int kGemmThreads = 32 * (kWarpDec0 + 4 * kDecPerQuarter);  // 1024
 constexpr int kUPS = 4;                            // units per ring stage
+constexpr int kCtrlRegs = 40;                      // setmaxnreg: control/epilogue warps
+constexpr int kDecRegs = 72;                       // setmaxnreg: decoder warps (64K regs total)
+constexpr int kRowBatch = 4;                       // FragTile rows decoded together per thread
+constexpr bool kLutSmem = true;                    // selector table in smem (LDS) vs constant bank (LDC)
 constexpr int kMaxCSlots = 8;
 constexpr int kMaxXSlots = 16;
 constexpr int kMaxASlots = 12;
 constexpr uint32_t kStageMeta = 128;               // see the stage header layout below
 constexpr uint32_t kStagePlanes = 2 * 3 * kUPS * 512;
 constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kRpWarp = 32 * 8 + 32;           // per decoder warp: 32 FragTiles x 8 rows (+ pad)
+constexpr uint32_t kRpTabBytes = 4 * kDecPerQuarter * kRpWarp;
 
 // stage header (u32 words): [4i+0..3] unit i {H a, H b, L a, L b} offsets inside the
 // stage regions; [16+q] ticket of lane quarter q; [20+i] unit i has BlockTile row b.
@@ -63,8 +69,8 @@ constexpr uint32_t kTmemCols = 512;
 struct __align__(8) Bars {
   uint64_t full_c[kMaxCSlots];
   uint64_t empty_c[kMaxCSlots];
-  uint64_t xfull[kMaxXSlots];
-  uint64_t decoded[kMaxASlots];
+  uint64_t xfull[kMaxXSlots / kUPS];     // per X-ring stage (4 tiles)
+  uint64_t decoded[kMaxASlots / kUPS];   // per A-ring stage (4 units x 4 quarters x 32 lanes)
   uint64_t mcommit[2];
   uint64_t accfull[2];
   uint64_t accempty[2];
@@ -104,14 +110,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // 1024-B alignment for the SW128 X tiles
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Bars* bars = reinterpret_cast<Bars*>(smem);
-  uint8_t* xslots = smem + 1024;
+  uint8_t* rptab = smem + 1024;                        // decoder row-prefix tables
+  uint4* slut = reinterpret_cast<uint4*>(smem + 1024 + kRpTabBytes);   // PRMT selector table
+  uint8_t* xslots = smem + 1024 + kRpTabBytes + 4096;
   uint8_t* cslots = xslots + (size_t)p.n_xslots * p.aslot_bytes;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const uint32_t S_c = p.n_cslots;
-  const uint32_t S_x = p.n_xslots;
-  const uint32_t S_a = p.n_aslots;
+  const uint32_t S_x = p.n_xslots;             // multiple of kUPS
+  const uint32_t S_a = p.n_aslots;             // multiple of kUPS
+  const uint32_t SXS = S_x / kUPS, SAS = S_a / kUPS;   // stage-granular rings
   const uint32_t capH = p.hcap, capL = p.lcap;
 
   // ---- stream-K range of this CTA (32-bit unit indices; the host checks the range)
@@ -125,13 +134,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t band0 = u0 / nbc, kc0 = u0 % nbc;
 
   // ---- setup
+  if (tid < 256) slut[tid] = c_lut[tid];
   if (tid == 32) {
     for (uint32_t i = 0; i < S_c; ++i) {
       mbar_init(&bars->full_c[i], 1);
       mbar_init(&bars->empty_c[i], 32 * 4 * kDecPerQuarter);
     }
-    for (uint32_t i = 0; i < S_x; ++i) mbar_init(&bars->xfull[i], 1);
-    for (uint32_t i = 0; i < S_a; ++i) mbar_init(&bars->decoded[i], 128);
+    for (uint32_t i = 0; i < S_x / kUPS; ++i) mbar_init(&bars->xfull[i], 1);
+    for (uint32_t i = 0; i < S_a / kUPS; ++i) mbar_init(&bars->decoded[i], 128 * kUPS);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->mcommit[i], 1);
       mbar_init(&bars->accfull[i], 1);
@@ -156,6 +166,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint64_t pol = policy_evict_first();
     const ulonglong2* off2 = reinterpret_cast<const ulonglong2*>(p.offsets);
     const int quad = lane >> 2, qi = lane & 3;
+    uint32_t slot = 0, eph = 1;   // ring slot / empty-barrier parity of the next stage
     for (int b0 = 0; b0 < nunits; b0 += 32) {
       const int it = b0 + lane;
       const bool valid = it < nunits;
@@ -201,9 +212,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t e_h1b = __shfl_sync(0xFFFFFFFFu, h1b, rend), e_l1b = __shfl_sync(0xFFFFFFFFu, l1b, rend);
       const uint32_t nrun = (uint32_t)(rend - lane + 1);
       const int st_hi = min(nstages, (b0 + 32) / kUPS);
-      for (int st = b0 / kUPS; st < st_hi; ++st) {
-        const uint32_t slot = (uint32_t)st % S_c;
-        mbar_wait(&bars->empty_c[slot], (((uint32_t)st / S_c) & 1u) ^ 1u);
+      for (int st = b0 / kUPS; st < st_hi; ++st, slot = (slot + 1 == S_c) ? 0u : slot + 1u, eph ^= (slot == 0)) {
+        mbar_wait(&bars->empty_c[slot], eph);
         uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
         const bool mine = (quad == st - b0 / kUPS);
         if (mine && valid) {
@@ -246,19 +256,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == kWarpProdX) {
     // ================================================================ activation producer
+    // per stage: the 4 X tiles of its units land on one barrier
     const uint64_t pol = policy_evict_last();
     const uint32_t xbytes = p.n_umma * 128u;
     uint32_t kc = kc0;
-    for (int it = 0; it < nunits; ++it) {
-      const uint32_t xs = (uint32_t)it % S_x;
-      // X slot xs is free once the MMAs of unit it - S_x have completed
-      wait_count(&bars->mma_done, (it >= (int)S_x) ? (uint32_t)(it - (int)S_x + 1) : 0u);
+    uint32_t xr = 0;   // X ring stage of st
+    for (int st = 0; st < nstages; ++st, xr = (xr + 1 == SXS) ? 0u : xr + 1u) {
+      // X ring stage xr is free once the MMAs of stage st - SXS have completed
+      wait_count(&bars->mma_done, (st >= (int)SXS) ? (uint32_t)((st - (int)SXS + 1) * kUPS) : 0u);
+      const int nu = min(kUPS, nunits - st * kUPS);
       if (elect_one()) {
-        mbar_arrive_expect_tx(&bars->xfull[xs], xbytes);
-        tma_load_2d(xslots + (size_t)xs * p.aslot_bytes, &xmap, (int32_t)(kc * 64), p.m0, &bars->xfull[xs], pol);
+        mbar_arrive_expect_tx(&bars->xfull[xr], xbytes * (uint32_t)nu);
+        uint32_t k = kc;
+        for (int i = 0; i < nu; ++i) {
+          tma_load_2d(xslots + (size_t)(xr * kUPS + i) * p.aslot_bytes, &xmap, (int32_t)(k * 64), p.m0,
+                      &bars->xfull[xr], pol);
+          if (++k == nbc) k = 0;
+        }
       }
       __syncwarp();
-      if (++kc == nbc) kc = 0;
+      kc += (uint32_t)nu;
+      if (kc >= nbc) kc -= nbc;
     }
   } else if (warp == kWarpMma) {
     // ================================================================ MMA issuer
@@ -280,6 +298,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     auto poll = [&](int issued) {
       while (pub < issued && mbar_test_wait(&bars->mcommit[pub & 1], ((uint32_t)pub >> 1) & 1u)) publish();
     };
+    // ring positions kept incrementally: no integer division on this warp's critical path
+    // (it shares its SM sub-partition with busy decoder warps, so every instruction counts)
+    uint32_t xs = 0, xph = 0, as_ = 0, aph = 0;   // X / A stage ring slot and phase
+    uint32_t xa = xbase, ta = tmem_a;             // X tile address / A slot column of the unit
+    const uint32_t xa_end = xbase + S_x * p.aslot_bytes, ta_end = tmem_a + 32u * S_a;
     for (int st = 0; st < nstages; ++st) {
       // at most two stages in flight (mcommit is a 2-deep ring observed in order)
       while (pub + 1 < st) {
@@ -287,11 +310,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         publish();
       }
       const int i0 = st * kUPS, i1 = min(nunits, i0 + kUPS);
-      for (int it = i0; it < i1; ++it) {
-        while (!mbar_test_wait(&bars->xfull[(uint32_t)it % S_x], ((uint32_t)it / S_x) & 1u)) poll(st);
-        while (!mbar_test_wait(&bars->decoded[(uint32_t)it % S_a], ((uint32_t)it / S_a) & 1u)) poll(st);
-      }
+      while (!mbar_test_wait(&bars->xfull[xs], xph)) poll(st);
+      while (!mbar_test_wait(&bars->decoded[as_], aph)) poll(st);
+      if (++xs == SXS) { xs = 0; xph ^= 1u; }
+      if (++as_ == SAS) { as_ = 0; aph ^= 1u; }
       tc_fence_after();
+      // fast path: a full stage strictly inside one accumulation segment -> 16 MMAs from one
+      // set of per-stage operands (the stage's A slots and X tiles are contiguous)
+      if (i1 - i0 == kUPS && i0 != 0 && i1 < nunits && kc != 0 && kc + kUPS < nbc) {
+        const uint32_t d = tmem_base + (uint32_t)(seg & 1) * dcols;
+        const uint64_t bdesc = umma_desc_sw128(xa);
+        const uint32_t bstep = p.aslot_bytes >> 4;   // descriptor address units per X tile
+        if (elect_one()) {
+#pragma unroll
+          for (int i = 0; i < kUPS; ++i) {
+            const uint64_t bd = bdesc + (uint64_t)(bstep * (uint32_t)i);
+            umma_bf16_ts(d, ta + 32u * i, bd, idesc, 1u);
+            umma_bf16_ts(d, ta + 32u * i + 8u, bd + 2, idesc, 1u);
+            umma_bf16_ts(d, ta + 32u * i + 16u, bd + 4, idesc, 1u);
+            umma_bf16_ts(d, ta + 32u * i + 24u, bd + 6, idesc, 1u);
+            trace_ev(p.trace, i0 + i, 6);
+          }
+          umma_commit(&bars->mcommit[st & 1]);
+        }
+        __syncwarp();
+        ta += 32u * kUPS; if (ta == ta_end) ta = tmem_a;
+        xa += kUPS * p.aslot_bytes; if (xa == xa_end) xa = xbase;
+        kc += kUPS;
+        poll(st + 1);
+        continue;
+      }
       for (int it = i0; it < i1; ++it) {
         const bool first = (it == 0) || (kc == 0);
         const bool last = (it == nunits - 1) || (kc + 1 == nbc);
@@ -301,8 +349,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tc_fence_after();
         }
         const uint32_t d = tmem_base + (uint32_t)(seg & 1) * dcols;
-        const uint32_t at = tmem_a + 32u * ((uint32_t)it % S_a);
-        const uint64_t bdesc = umma_desc_sw128(xbase + ((uint32_t)it % S_x) * p.aslot_bytes);
+        const uint32_t at = ta;
+        const uint64_t bdesc = umma_desc_sw128(xa);
+        ta += 32u; if (ta == ta_end) ta = tmem_a;
+        xa += p.aslot_bytes; if (xa == xa_end) xa = xbase;
         if (elect_one()) {
           umma_bf16_ts(d, at, bdesc, idesc, first ? 0u : 1u);
           umma_bf16_ts(d, at + 8u, bdesc + 2, idesc, 1u);
@@ -329,28 +379,43 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int lr = lane + 32 * hh;                // row inside the BlockTile
     const int fr = lr >> 3, r8 = lr & 7;
     const int tr = fr >> 1;                       // TensorCoreTile row of this thread's FragTiles
-    const uint32_t bsel = (uint32_t)(r8 & 3) | 0x4440u;
-    const bool hi_row = r8 >= 4;
     const uint32_t obase = (uint32_t)(tr * 16 + (fr & 1));                 // o for fc = 0
-    const uint32_t hoff = (uint32_t)((r8 >> 2) << 2);                      // plane half of the row
     const int srcbase = (tr - 2 * hh) * 16 + (fr & 1);
     const uint32_t tq = tmem_a + ((uint32_t)(32 * q) << 16);
     const int fo = 32 * hh + lane;                // scan lane's FragTile
-    for (int st = 0; st < nstages; ++st) {
-      const uint32_t slot = (uint32_t)st % S_c;
-      mbar_wait(&bars->full_c[slot], ((uint32_t)st / S_c) & 1u);
+    // row-prefix table of this warp: FragTile o (local 0..31) at o*8 + (o >> 4)*16 (the pad
+    // keeps the 4 FragTiles a warp reads at once on distinct banks)
+    uint8_t* rpt = rptab + (warp - kWarpDec0) * kRpWarp;
+    const uint32_t rp_wr = (uint32_t)lane * 8u + ((uint32_t)lane >> 4) * 16u;
+    const uint32_t ol0 = obase - 32u * hh;        // local FragTile index for fc = 0
+    // The decoded-barrier arrival of a unit is deferred until after the next unit's scan,
+    // so the tcgen05.st completion wait overlaps useful work.
+    int pend = -1;                                // A-ring stage of the pending arrival, -1 = none
+    auto flush = [&]() {
+      if (pend >= 0) {
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bars->decoded[pend]);
+        pend = -1;
+      }
+    };
+    uint32_t slot = 0, cph = 0, astg = 0;         // C ring slot / phase, A ring stage (no divisions)
+    for (int st = 0; st < nstages; ++st, slot = (slot + 1 == S_c) ? 0u : slot + 1u, cph ^= (slot == 0),
+             astg = (astg + 1 == SAS) ? 0u : astg + 1u) {
+      mbar_wait(&bars->full_c[slot], cph);
       const uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
       const uint32_t* meta = reinterpret_cast<const uint32_t*>(cs);
       uint32_t* tickets = const_cast<uint32_t*>(meta) + 16;
       const int nu = min(kUPS, nunits - st * kUPS);
-      while (true) {
+      while (true) {   // 4 tickets per quarter and stage (tickets >= nu only arrive)
         uint32_t j = 0;
         if (lane == 0) j = atomicAdd(&tickets[q], 1u);
         j = shfl_idx(j, 0);
-        if ((int)j >= nu) break;
+        if ((int)j >= kUPS) break;
         const int it = st * kUPS + (int)j;
-        const uint32_t a = (uint32_t)it % S_a;
-        const bool present = (bt_sel == 0) || (meta[20 + j] != 0u);
+        const uint32_t a = astg * kUPS + j;   // A slot of this unit
+        const bool present = ((int)j < nu) && ((bt_sel == 0) || (meta[20 + j] != 0u));
+        if (lane == 0 && (int)j < nu) trace_ev(p.trace, it, 7 + q);
         if (present) {
           const uint4 mt = *reinterpret_cast<const uint4*>(meta + 4 * j);  // {H a, H b, L a, L b}
           const uint8_t* P1 = cs + kStageMeta + (bt_sel * 3) * (kUPS * 512) + j * 512;
@@ -383,41 +448,55 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t bl = bytepop(mlo), bh = bytepop(mhi);
           const uint32_t rp_lo = bl * 0x01010100u;
           const uint32_t rp_hi = bh * 0x01010100u + ((bl * 0x01010101u) >> 24) * 0x01010101u;
-          // A slot a must be free: the MMAs of unit it - S_a have completed
-          wait_count(&bars->mma_done, (it >= (int)S_a) ? (uint32_t)(it - (int)S_a + 1) : 0u);
+          __syncwarp();   // previous unit's readers are done
+          *reinterpret_cast<uint2*>(rpt + rp_wr) = make_uint2(rp_lo, rp_hi);
+          __syncwarp();
+          flush();
+          // A slot a must be free: the MMAs of stage st - SAS have completed
+          wait_count(&bars->mma_done, (st >= (int)SAS) ? (uint32_t)((st - (int)SAS + 1) * kUPS) : 0u);
           tc_fence_after();
+          if (lane == 0) trace_ev(p.trace, it, 11 + q);
           const uint32_t taddr0 = tq + 32u * a;
+          // Absolute smem byte offsets (relative to `smem`) so every per-row address is a
+          // per-unit base plus an immediate.  FragTile of row f: o = obase + cf(f),
+          // cf(f) = (f>>1)*4 + (f&1)*2 (canonical order of FragTile column f).
+          const uint32_t hb = (uint32_t)(H - smem);                     // 16-B aligned
+          const uint32_t pexcl = excl + hb;                             // FragTile H start, absolute
+          const uint8_t* pb = P1 + obase * 8u + (uint32_t)r8;           // this row's plane byte, f = 0
+          const uint8_t* rb = rpt + ol0 * 8u + (ol0 >> 4) * 16u + (uint32_t)r8;
+          const uint32_t la0 = (uint32_t)((const uint8_t*)L - smem) + 2u * hb +
+                               16u * (obase * 8u + (uint32_t)r8);      // + 128 cf(f) - 2 hs_abs
 #pragma unroll
-          for (int fb = 0; fb < 8; fb += 4) {
-            uint4 v[4];
+          for (int fb = 0; fb < 8; fb += kRowBatch) {
+            uint4 v[kRowBatch];
 #pragma unroll
-            for (int qq = 0; qq < 4; ++qq) {
+            for (int qq = 0; qq < kRowBatch; ++qq) {
               const int f = fb + qq;
-              const int src = srcbase + (f >> 1) * 4 + (f & 1) * 2;
-              const uint32_t pref = shfl_idx(excl, src);
-              const uint32_t rl = shfl_idx(rp_lo, src);
-              const uint32_t rh = shfl_idx(rp_hi, src);
-              const uint32_t hs = pref + prmt(hi_row ? rh : rl, 0u, bsel);
-              const uint32_t o = obase + (uint32_t)((f >> 1) * 4 + (f & 1) * 2);
-              const uint32_t ls = (o * 8u + (uint32_t)r8) * 8u - hs;
-              const uint32_t off = o * 8u + hoff;
-              const uint32_t b1 = prmt(*reinterpret_cast<const uint32_t*>(P1 + off), 0u, bsel);
-              const uint32_t b2 = prmt(*reinterpret_cast<const uint32_t*>(P2 + off), 0u, bsel);
-              const uint32_t b3 = prmt(*reinterpret_cast<const uint32_t*>(P3 + off), 0u, bsel);
+              const uint32_t cf = (uint32_t)((f >> 1) * 4 + (f & 1) * 2);
+              const uint32_t hs_abs = shfl_idx(pexcl, srcbase + (int)cf) + rb[cf * 8u];
+              const uint32_t b1 = pb[cf * 8u];
+              const uint32_t b2 = pb[cf * 8u + kUPS * 512];
+              const uint32_t b3 = pb[cf * 8u + 2 * kUPS * 512];
               const uint32_t m = b1 | b2 | b3;
-              v[qq] = decode_row_core(b1, b2, b3, m, c_lut[m], H, hs, L, ls, p.eb7x2);
+              v[qq] = decode_row_abs(b1, b2, b3, m, slut[m],
+                                     reinterpret_cast<const uint32_t*>(smem + (hs_abs & ~3u)), hs_abs * 8u,
+                                     reinterpret_cast<const uint16_t*>(smem + mad_lo(hs_abs, ZS_MUL(kMNeg2, 0xFFFFFFFEu), la0 + 128u * cf)),
+                                     p.eb7x2);
             }
-            tmem_st8(taddr0 + 4u * fb, v[0], v[1]);
-            tmem_st8(taddr0 + 4u * fb + 8u, v[2], v[3]);
+#pragma unroll
+            for (int qq = 0; qq < kRowBatch; qq += 2) tmem_st8(taddr0 + 4u * (fb + qq), v[qq], v[qq + 1]);
           }
-          tmem_wait_st();
+          pend = (int)astg;
+          if (lane == 0) trace_ev(p.trace, it, 2 + q);
+        } else {
+          flush();
+          tc_fence_before();
+          mbar_arrive(&bars->decoded[astg]);
         }
-        tc_fence_before();
-        mbar_arrive(&bars->decoded[a]);
-        if (lane == 0) trace_ev(p.trace, it, 2 + q);
       }
-      mbar_arrive(&bars->empty_c[slot]);
+      mbar_arrive(&bars->empty_c[slot]);   // this warp no longer reads the stage's smem
     }
+    flush();
   } else if (warp >= kWarpEpi0) {
     // ================================================================ epilogue (warps 4..7)
     const int et = tid - 32 * kWarpEpi0;  // 0..127 = TMEM lane = row inside the band
@@ -497,7 +576,8 @@ cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, 
 }
 
 size_t gemm_smem_bytes(const GemmParams& p) {
-  return 1024 /*align slack*/ + 1024 + (size_t)p.n_xslots * p.aslot_bytes + (size_t)p.n_cslots * p.cslot_bytes;
+  return 1024 /*align slack*/ + 1024 + kRpTabBytes + 4096 + (size_t)p.n_xslots * p.aslot_bytes +
+         (size_t)p.n_cslots * p.cslot_bytes;
 }
 
 int gemm_threads() { return kGemmThreads; }
@@ -507,5 +587,6 @@ int gemm_max_aslots() { return kMaxASlots; }
 uint32_t gemm_stage_fixed_bytes() { return kStageMeta + kStagePlanes; }
 int gemm_units_per_stage() { return kUPS; }
 int gemm_max_chunk() { return 128; }
+uint32_t gemm_fixed_smem() { return 1024 + 1024 + kRpTabBytes + 4096; }
 
 }  // namespace zs

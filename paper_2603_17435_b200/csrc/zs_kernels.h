@@ -67,5 +67,6 @@ int gemm_max_aslots();
 uint32_t gemm_stage_fixed_bytes();
 int gemm_units_per_stage();
 int gemm_max_chunk();
+uint32_t gemm_fixed_smem();
 
 }  // namespace zs

@@ -20,14 +20,36 @@ x = torch.randn(M, K, device=dev).to(torch.bfloat16)
 tr = torch.zeros(4 * 128 * 16, dtype=torch.int64, device=dev)
 L = Z.lib()
 L.zs_debug_set_trace.argtypes = [ctypes.c_void_p]
+L.zs_debug_set_ring.argtypes = [ctypes.c_int]
+if len(sys.argv) > 3:
+    L.zs_debug_set_ring(int(sys.argv[3]))
 for _ in range(3):
     Z.gemm(x, wd)
 L.zs_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
 Z.gemm(x, wd)
 torch.cuda.synchronize()
 L.zs_debug_set_trace(None)
-t = tr.cpu().numpy().reshape(4, 128, 16).astype(np.int64)[:, :, :7]
-names = ["prod", "-", "dq0", "dq1", "dq2", "dq3", "mma"]
+t = tr.cpu().numpy().reshape(4, 128, 16).astype(np.int64)[:, :, :15]
+names = ["prod", "-", "dq0", "dq1", "dq2", "dq3", "mma", "tk0", "tk1", "tk2", "tk3", "as0", "as1", "as2", "as3"]
+# summary over the first 4 CTAs: decode duration (slot-acquired -> done) and ticket->done
+d1, d2 = [], []
+for cta in range(4):
+    for u in range(128):
+        r = t[cta, u]
+        for q in range(4):
+            if r[2 + q] and r[11 + q]:
+                d1.append(r[2 + q] - r[11 + q])
+            if r[2 + q] and r[7 + q]:
+                d2.append(r[2 + q] - r[7 + q])
+print("decode (A slot ready -> done) cycles: mean %.0f  p10 %.0f  p90 %.0f" % (np.mean(d1), np.percentile(d1, 10), np.percentile(d1, 90)))
+print("ticket -> done cycles: mean %.0f" % np.mean(d2))
+for cta in range(4):
+    r = t[cta]
+    nz = r[r > 0]
+    last_mma = r[:, 6].max()
+    first = nz.min()
+    n = int((r[:, 6] > 0).sum())
+    print(f"CTA {cta}: units traced {n}, span first->last MMA {last_mma - first} cycles, per unit {(last_mma - first) / max(n, 1):.0f}")
 for cta in range(1):
     base = t[cta][t[cta] > 0].min()
     print(f"CTA {cta}: times in cycles relative to first event")

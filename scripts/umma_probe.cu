@@ -8,7 +8,9 @@
 
 using namespace zs;
 
-__global__ void probe(int n_mma, uint32_t N, int ts, int nacc, unsigned long long* out) {
+__device__ volatile int g_stop;
+
+__global__ void probe(int n_mma, uint32_t N, int ts, int nacc, unsigned long long* out, int st_warps) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
@@ -24,6 +26,19 @@ __global__ void probe(int n_mma, uint32_t N, int ts, int nacc, unsigned long lon
   tc_fence_after();
   const uint32_t t0 = tbase;
   unsigned long long c0 = 0, c1 = 0, c2 = 0;
+  __shared__ volatile int stop;
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  const int w = threadIdx.x >> 5;
+  if (w >= 4 && w < 4 + st_warps) {   // background tcgen05.st traffic into columns 384..511
+    const uint32_t ta = t0 + ((uint32_t)(32 * (w & 3)) << 16) + 384u + 8u * ((w >> 2) & 15);
+    uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
+    while (!stop) {
+      for (int r = 0; r < 16; ++r) tmem_st8(ta, v, v);
+      tmem_wait_st();
+      v.x += 1;
+    }
+  }
   if (threadIdx.x < 32) {   // whole warp runs the loop; one elected lane issues
     const uint32_t idesc = umma_idesc_bf16(128, N);
     const uint32_t a_s = smem_u32(base), b_s = smem_u32(base + 32768);
@@ -62,6 +77,7 @@ __global__ void probe(int n_mma, uint32_t N, int ts, int nacc, unsigned long lon
     if (threadIdx.x == 0) {
       out[0] = c1 - c0;
       out[1] = c2 - c0;
+      stop = 1;
     }
   }
   tc_fence_before();
@@ -76,11 +92,13 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 16);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
-  for (int ts = 0; ts < 2; ++ts)
-    for (uint32_t N : {16u, 32u, 64u})
-      for (int nacc : {1, 8})
-      for (int n : {4, 16, 512}) {
-        probe<<<1, 128, 70 * 1024>>>(n, N, ts, nacc, d);
+  for (int stw : {0, 8, 16, 24})
+  for (int ts = 1; ts < 2; ++ts)
+    for (uint32_t N : {32u})
+      for (int nacc : {8})
+      for (int n : {512}) {
+        printf("st_warps=%d ", stw);
+        probe<<<1, 128 + 32 * (stw + 4), 70 * 1024>>>(n, N, ts, nacc, d, stw);
         unsigned long long h[2];
         cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
         printf("nacc=%d ", nacc);
