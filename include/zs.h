@@ -127,7 +127,7 @@ size_t zs_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
  * memory and BF16 output (RNE).  x: device BF16, row-major, leading dimension ldx
  * (elements), base 16-byte aligned and ldx*2 % 16 == 0 (TMA rule).  w: DEVICE tensor with
  * w->sz.rows == N, w->sz.cols == K.  y: device BF16 [M][ldy], ldy >= N.  Outputs of
- * padded rows are not written.  M >= 1 (any size; M > 256 is processed in 256-token
+ * padded rows are not written.  M >= 1 (any size; M > 128 is processed in 128-token
  * chunks, each re-decoding W).  workspace: see zs_gemm_workspace_bytes.
  * Errors: ZS_ERR_INVALID_ARG, ZS_ERR_SHAPE, ZS_ERR_ALIGNMENT, ZS_ERR_CAPACITY
  * (workspace too small), ZS_ERR_UNSUPPORTED, ZS_ERR_CUDA. */

@@ -10,5 +10,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --set full --clock-control none --import-source on -k regex:zipgemm -s 4 -c 1 -f -o gpurun_out/prof_${TAG} \
     python bench.py --steps 5 --warmup 2 --m $M --no-extras --no-cpu-baseline > gpurun_out/prof_${TAG}.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:decompress -s 2 -c 1 -f -o gpurun_out/prof_decomp_${TAG} \
-    python scripts/decomp_bench.py --iters 5 > gpurun_out/prof_decomp_${TAG}.log 2>&1
+    python scripts/decomp_bench.py --iters 5 --layers L8B.GateUp > gpurun_out/prof_decomp_${TAG}.log 2>&1
 ls -la gpurun_out
