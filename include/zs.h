@@ -117,18 +117,36 @@ zs_status zs_encode(const uint16_t *w, int64_t rows, int64_t cols, int64_t ld, i
  * ZS_ERR_CUDA. */
 zs_status zs_decompress(const zs_tensor *w, uint16_t *out, int64_t ld_out, void *stream);
 
-/* Workspace (device bytes) zs_gemm needs for an M x N x K problem: fp32 split-K partial
- * sums [M][N] plus per-band arrival counters.  The workspace must be zero-filled once
- * before its first use; zs_gemm leaves it zero-filled again when it completes, so one
- * workspace can be reused by every later call on the same stream. */
+/* Token count above which zs_gemm takes the decoupled prefill path ("decoupled
+ * decompression + dense GEMM for the compute-bound prefill stage"): zs_decompress of W
+ * into the workspace, then one dense BF16 tensor-core GEMM (cuBLAS, fp32 accumulate).
+ * At or below it the fused ZipGEMM kernel runs (decode stage).  Value measured on B200,
+ * see DESIGN.md (crossover of the two paths over LLaMA-3.1-8B layer shapes). */
+#define ZS_GEMM_LARGE_M 128
+
+/* Workspace (device bytes) zs_gemm needs for an M x N x K problem.
+ *   M <= ZS_GEMM_LARGE_M: fp32 split-K partial sums [M][N] plus per-band arrival
+ *     counters.  It must be zero-filled once before its first use; zs_gemm leaves it
+ *     zero-filled again when it completes, so one workspace can be reused by every later
+ *     call on the same stream.
+ *   M >  ZS_GEMM_LARGE_M: scratch for the decoded weight, N x roundup(K, 8) BF16.  Any
+ *     contents on entry; NOT zero on exit, so do not hand the same buffer to a fused
+ *     call afterwards without zero-filling it (zs_gemm_is_decoupled tells the paths apart).
+ * Returns 0 for non-positive sizes. */
 size_t zs_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+
+/* 1 if zs_gemm takes the decoupled path for this token count (M > ZS_GEMM_LARGE_M), else
+ * 0.  Host, O(1), no errors. */
+int zs_gemm_is_decoupled(int64_t M);
 
 /* ZipGEMM: Y[M][N] = X[M][K] * W[N][K]^T with fp32 accumulation in tensor
  * memory and BF16 output (RNE).  x: device BF16, row-major, leading dimension ldx
  * (elements), base 16-byte aligned and ldx*2 % 16 == 0 (TMA rule).  w: DEVICE tensor with
  * w->sz.rows == N, w->sz.cols == K.  y: device BF16 [M][ldy], ldy >= N.  Outputs of
- * padded rows are not written.  M >= 1 (any size; M > 128 is processed in 128-token
- * chunks, each re-decoding W).  workspace: see zs_gemm_workspace_bytes.
+ * padded rows are not written.  M >= 1: M <= ZS_GEMM_LARGE_M runs the fused kernel (one
+ * launch); larger M runs zs_decompress + a cuBLAS BF16 GEMM on the same stream (the
+ * library keeps one cuBLAS handle per host thread and device, created on first use).
+ * workspace: see zs_gemm_workspace_bytes.
  * Errors: ZS_ERR_INVALID_ARG, ZS_ERR_SHAPE, ZS_ERR_ALIGNMENT, ZS_ERR_CAPACITY
  * (workspace too small), ZS_ERR_UNSUPPORTED, ZS_ERR_CUDA. */
 zs_status zs_gemm(const uint16_t *x, int64_t ldx, const zs_tensor *w, uint16_t *y, int64_t ldy,

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <cublas_v2.h>
 
 #include <algorithm>
 #include <cstring>
@@ -16,7 +17,20 @@ namespace {
 
 thread_local int g_last_launches = 0;
 unsigned long long* g_trace = nullptr;  // debug: set by zs_debug_set_trace
+uint32_t g_dbg = 0;                     // debug: experiment flags (zs_debug_set_flags)
 uint32_t g_max_cslots = 3;              // ring depth cap (tunable via zs_debug_set_ring)
+int64_t g_large_m = ZS_GEMM_LARGE_M;    // decoupled-path threshold (zs_debug_set_large_m)
+
+// cuBLAS handle of the decoupled prefill path: one per (host thread, device), created on
+// first use.  cuBLAS only runs the plain dense GEMM on the already-decoded weights.
+cublasHandle_t blas_handle(int dev) {
+  thread_local cublasHandle_t h[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!h[dev] && cublasCreate(&h[dev]) != CUBLAS_STATUS_SUCCESS) h[dev] = nullptr;
+  return h[dev];
+}
+
+bool use_decoupled(int64_t M) { return M > g_large_m; }
 
 inline int64_t up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -96,7 +110,12 @@ extern "C" int zs_last_launch_count(void) { return g_last_launches; }
 // Debug hook (not part of include/zs.h): device buffer of 4*128*16 u64 for per-unit
 // pipeline timestamps of the first 4 CTAs of subsequent zs_gemm launches; NULL disables.
 extern "C" void zs_debug_set_trace(unsigned long long* dev_buf) { g_trace = dev_buf; }
+// Debug hook: 1 = decoders skip the row decode, 2 = skip tcgen05.st, 4 = no tcgen05.mma
+// (timing experiments only: results are wrong with any flag set).
+extern "C" void zs_debug_set_flags(int flags) { g_dbg = (uint32_t)flags; }
 extern "C" void zs_debug_set_ring(int max_cslots) { g_max_cslots = (uint32_t)std::max(1, max_cslots); }
+// Debug hook: move the fused / decoupled threshold (crossover measurement); < 0 restores it.
+extern "C" void zs_debug_set_large_m(long long m) { g_large_m = m < 0 ? ZS_GEMM_LARGE_M : (int64_t)m; }
 
 extern "C" zs_status zs_decompress(const zs_tensor* w, uint16_t* out, int64_t ld_out, void* stream) {
   g_last_launches = 0;
@@ -124,23 +143,33 @@ extern "C" zs_status zs_decompress(const zs_tensor* w, uint16_t* out, int64_t ld
   p.stage_bytes = (uint32_t)up(1536 + p.hcap + lcap, 128);
   p.eb7x2 = eb7x2_of(w->base_exp);
   p.vec_ok = aligned16(out) && (ld_out % 8 == 0);
-  const size_t smem = zs::decompress_smem_bytes(p.stage_bytes);
-  int per_sm = (int)std::min<size_t>(8, (220 * 1024) / (smem + 1024));
-  per_sm = std::max(per_sm, 1);
-  const int64_t grid = std::min<int64_t>(p.n_blocktiles, (int64_t)sms * per_sm);
-  cudaError_t e = zs::launch_decompress(p, (int)grid, smem, (cudaStream_t)stream);
+  // one CTA per SM; as many independent decoder warps (2 stages each) as fit in smem
+  int warps = zs::decompress_max_warps();
+  while (warps > 1 && zs::decompress_smem_bytes(p.stage_bytes, warps) > 227 * 1024) --warps;
+  if (zs::decompress_smem_bytes(p.stage_bytes, warps) > 227 * 1024) return ZS_ERR_UNSUPPORTED;
+  const size_t smem = zs::decompress_smem_bytes(p.stage_bytes, warps);
+  const int64_t grid = std::min<int64_t>((p.n_blocktiles + warps - 1) / warps, (int64_t)sms);
+  cudaError_t e = zs::launch_decompress(p, (int)grid, warps, smem, (cudaStream_t)stream);
   if (e != cudaSuccess) return ZS_ERR_CUDA;
   g_last_launches = 1;
   return ZS_OK;
 }
 
-extern "C" size_t zs_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
-  (void)K;
-  if (M < 1 || N < 1) return 0;
+// split-K region: fp32 partials [min(M,256)][N] + per-band counters (zero between calls)
+static size_t splitk_bytes(int64_t M, int64_t N) {
   const int64_t mc = std::min<int64_t>(M, 256);
   const int64_t nbands = (up(N, 64) / 64 + 1) / 2;
-  return (size_t)(mc * N * 4) + (size_t)up(nbands * 4, 256);
+  return (size_t)up(mc * N * 4 + up(nbands * 4, 256), 256);
 }
+
+extern "C" size_t zs_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+  if (M < 1 || N < 1 || K < 1) return 0;
+  // decoupled path: scratch for the decoded W [N][roundup(K,8)] bf16
+  if (use_decoupled(M)) return (size_t)up(N * up(K, 8) * 2, 256);
+  return splitk_bytes(M, N);
+}
+
+extern "C" int zs_gemm_is_decoupled(int64_t M) { return use_decoupled(M) ? 1 : 0; }
 
 extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w, uint16_t* y, int64_t ldy, int64_t M,
                              int64_t N, int64_t K, void* workspace, size_t workspace_bytes, void* stream) {
@@ -155,6 +184,29 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
   if (!aligned16(workspace)) return ZS_ERR_ALIGNMENT;
   int sms = 0;
   if ((st = device_check(&sms)) != ZS_OK) return st;
+
+  if (use_decoupled(M)) {
+    // Large M (prefill): ZipServ-Decomp into the workspace, then a dense BF16 GEMM
+    // on the tensor cores (cuBLAS).  The decode runs once per call instead of once per
+    // 128-token chunk.
+    const int64_t ldw = up(K, 8);
+    uint16_t* wdense = reinterpret_cast<uint16_t*>(workspace);
+    if ((st = zs_decompress(w, wdense, ldw, stream)) != ZS_OK) return st;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cublasHandle_t h = blas_handle(dev);
+    if (!h || cublasSetStream(h, (cudaStream_t)stream) != CUBLAS_STATUS_SUCCESS) return ZS_ERR_CUDA;
+    if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return ZS_ERR_UNSUPPORTED;
+    const float one = 1.0f, zero = 0.0f;
+    // column-major view: Y^T[N][M] = W[N][K] (op T of the K x N col-major W) * X^T[K][M]
+    cublasStatus_t bs = cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)N, (int)M, (int)K, &one, wdense,
+                                     CUDA_R_16BF, (int)ldw, x, CUDA_R_16BF, (int)ldx, &zero, y, CUDA_R_16BF,
+                                     (int)ldy, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+    if (bs != CUBLAS_STATUS_SUCCESS) return ZS_ERR_CUDA;
+    g_last_launches = 1;   // our kernels only (the cuBLAS GEMM is library code)
+    return ZS_OK;
+  }
+
   auto enc = get_encode_tiled();
   if (!enc) return ZS_ERR_UNSUPPORTED;
 
@@ -185,6 +237,7 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
   }
   p.eb7x2 = eb7x2_of(w->base_exp);
   p.trace = g_trace;
+  p.dbg = g_dbg;
 
   // X tensor map: dims {K, M}, row stride ldx*2 bytes, box {64, n_umma}, SWIZZLE_128B;
   // out-of-bounds rows/columns are zero-filled by the TMA unit.
@@ -224,6 +277,9 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
     uint32_t na = (512u - 2u * p.acc_cols) / 32u;
     na = std::min<uint32_t>(na, (uint32_t)zs::gemm_max_aslots());
     p.n_aslots = na - na % 4;
+    auto magic = [](uint32_t d) { return d <= 1u ? 0u : (uint32_t)((1ull << 32) / d + 1ull); };
+    p.cdiv_magic = magic(p.n_cslots);
+    p.adiv_magic = magic(p.n_aslots);
     if (p.n_umma != cur_box) {
       cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
       cuuint64_t strides[1] = {(cuuint64_t)(ldx * 2)};

@@ -1,99 +1,140 @@
 // zs_decompress.cu -- ZipServ-Decomp on sm_100a.
 //
-// Persistent CTAs walk BlockTiles (64x64).  Per BlockTile the compressed bytes (three
-// 512-B plane slices, the H and L segments) arrive by 1-D TMA bulk copies into a
-// double-buffered smem stage; warp 0 scans the 64 FragTile popcounts (the paper's
-// __popc/__shfl_sync addressing); every thread then decodes two FragTile rows
-// with the shared branch-free row decoder and writes 16 B of BF16 to global memory
-// (8 consecutive threads = one 128-B row segment, fully coalesced).
+// HBM-bound: reads 1.40 B and writes 2 B per weight element (8B GateUp: 165 MB in, 235 MB
+// out).  Design: one persistent CTA per SM, every WARP is an independent decoder with its
+// own double-buffered smem stage and mbarriers, so there is no CTA-wide barrier anywhere.
+//
+//   warp g (of G = grid x warps) decodes BlockTiles g, g + G, ...  Per BlockTile:
+//   1. lane 0 issues the 1-D TMA bulk copies of the NEXT BlockTile (3 plane slices, the H
+//      and L segments) into the other stage: one load in flight per warp while it decodes.
+//   2. scan: lane l owns FragTiles 2l, 2l+1; popcounts of M = B1|B2|B3, a warp
+//      prefix scan over the 64 FragTiles, and per-row byte prefixes -> the H start of every
+//      FragTile row, stored as u16 in a bank-spread table [r8][o].
+//   3. 16 passes of 32 rows: lane -> (row lr = 4 pass + lane/8, FragTile column lane%8),
+//      the branch-free row decoder of zs_device.cuh, and one 16-B store per lane (8 lanes =
+//      one 128-B row segment, fully coalesced).
 #include "zs_device.cuh"
 #include "zs_kernels.h"
+#include "zs_lut.h"
 
 namespace zs {
 
-constexpr int kDecompThreads = 256;
+constexpr int kDecompMaxWarps = 16;
+constexpr uint32_t kHsRow = 80;                  // u16 per r8 row of the H-start table
+constexpr uint32_t kHsTabBytes = 8 * kHsRow * 2;  // 1280 B per warp
 
-__global__ void __launch_bounds__(kDecompThreads) decompress_kernel(DecompParams p) {
+__global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(DecompParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint4* lut = reinterpret_cast<uint4*>(smem);                        // 4 KB
-  uint32_t* ftpref = reinterpret_cast<uint32_t*>(smem + 4096);        // 64 x u32
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 4096 + 256);    // 2 mbarriers
-  uint8_t* stage_base = smem + 4096 + 256 + 64;
+  uint4* lut = reinterpret_cast<uint4*>(smem);   // 4 KB selector table
+  const int nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 4096) + 2 * warp;
+  uint16_t* hst = reinterpret_cast<uint16_t*>(smem + 4096 + 16 * kDecompMaxWarps + warp * kHsTabBytes);
+  uint8_t* stage0 = smem + 4096 + 16 * kDecompMaxWarps + kDecompMaxWarps * kHsTabBytes +
+                    (size_t)warp * 2 * p.stage_bytes;
   const uint32_t stage_bytes = p.stage_bytes;
 
-  const int tid = threadIdx.x;
-  lut[tid] = build_lut_entry((uint32_t)tid);
-  if (tid == 0) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = c_lut[i];
+  if (lane == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     fence_mbar_init();
   }
-  __syncthreads();
+  __syncthreads();   // lut visible (the only CTA-wide barrier)
 
   const int64_t nbt = p.n_blocktiles;
+  const int64_t G = (int64_t)gridDim.x * nw;
   const uint64_t pol = policy_evict_first();
   auto issue = [&](int64_t bt, int s) {
-    uint8_t* st = stage_base + (size_t)s * stage_bytes;
-    const uint64_t h0 = p.offsets[2 * bt], h1 = p.offsets[2 * bt + 2];
-    const uint64_t l0 = p.offsets[2 * bt + 1], l1 = p.offsets[2 * bt + 3];
-    const uint32_t hb = (uint32_t)(h1 - h0), lb = (uint32_t)(l1 - l0);
+    uint8_t* st = stage0 + (size_t)s * stage_bytes;
+    const ulonglong2 a = reinterpret_cast<const ulonglong2*>(p.offsets)[bt];
+    const ulonglong2 b = reinterpret_cast<const ulonglong2*>(p.offsets)[bt + 1];
+    const uint32_t hb = (uint32_t)(b.x - a.x), lb = (uint32_t)(b.y - a.y);
     mbar_arrive_expect_tx(&bars[s], 1536u + hb + lb);
     bulk_g2s(st, p.b1 + bt * 64, 512, &bars[s], pol);
     bulk_g2s(st + 512, p.b2 + bt * 64, 512, &bars[s], pol);
     bulk_g2s(st + 1024, p.b3 + bt * 64, 512, &bars[s], pol);
-    if (hb) bulk_g2s(st + 1536, p.h + h0, hb, &bars[s], pol);
-    if (lb) bulk_g2s(st + 1536 + p.hcap, reinterpret_cast<const uint8_t*>(p.l) + l0, lb, &bars[s], pol);
+    if (hb) bulk_g2s(st + 1536, p.h + a.x, hb, &bars[s], pol);
+    if (lb) bulk_g2s(st + 1536 + p.hcap, reinterpret_cast<const uint8_t*>(p.l) + a.y, lb, &bars[s], pol);
   };
 
-  int64_t bt = blockIdx.x;
-  if (tid == 0 && bt < nbt) issue(bt, 0);
-  uint32_t it = 0;
-  for (; bt < nbt; bt += gridDim.x, ++it) {
+  int64_t bt = (int64_t)blockIdx.x * nw + warp;
+  if (lane == 0 && bt < nbt) issue(bt, 0);
+  __syncwarp();
+
+  // per-lane constants of the row passes
+  const int fc = lane & 7;                                  // FragTile column (K / 8)
+  const uint32_t ofc = (uint32_t)((fc >> 1) * 4 + (fc & 1) * 2);
+  const uint32_t smem_base = smem_u32(smem);
+  (void)smem_base;
+  const uint32_t eb7x2 = p.eb7x2;
+
+  for (uint32_t it = 0; bt < nbt; bt += G, ++it) {
     const int s = it & 1;
-    const int64_t nxt = bt + gridDim.x;
-    if (tid == 0 && nxt < nbt) issue(nxt, s ^ 1);  // stage s^1 was released by the last barrier
+    const int64_t nxt = bt + G;
+    if (lane == 0 && nxt < nbt) issue(nxt, s ^ 1);   // stage s^1 was consumed last iteration
     mbar_wait(&bars[s], (it >> 1) & 1);
 
-    const uint8_t* st = stage_base + (size_t)s * stage_bytes;
-    const uint64_t* P1 = reinterpret_cast<const uint64_t*>(st);
-    const uint64_t* P2 = P1 + 64;
-    const uint64_t* P3 = P1 + 128;
+    const uint8_t* st = stage0 + (size_t)s * stage_bytes;
     const uint8_t* H = st + 1536;
     const uint16_t* L = reinterpret_cast<const uint16_t*>(st + 1536 + p.hcap);
 
-    // FragTile prefix popcounts in canonical order (warp 0, two FragTiles per lane)
-    if (tid < 32) {
-      const uint32_t c0 = __popcll(P1[2 * tid] | P2[2 * tid] | P3[2 * tid]);
-      const uint32_t c1 = __popcll(P1[2 * tid + 1] | P2[2 * tid + 1] | P3[2 * tid + 1]);
+    // ---- scan: FragTiles 2*lane, 2*lane+1 (canonical order)
+    {
+      const uint4 a1 = *reinterpret_cast<const uint4*>(st + 16 * lane);
+      const uint4 a2 = *reinterpret_cast<const uint4*>(st + 512 + 16 * lane);
+      const uint4 a3 = *reinterpret_cast<const uint4*>(st + 1024 + 16 * lane);
+      const uint32_t m0l = a1.x | a2.x | a3.x, m0h = a1.y | a2.y | a3.y;
+      const uint32_t m1l = a1.z | a2.z | a3.z, m1h = a1.w | a2.w | a3.w;
+      const uint32_t c0 = __popc(m0l) + __popc(m0h), c1 = __popc(m1l) + __popc(m1h);
       uint32_t incl = c0 + c1;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-        if (tid >= d) incl += v;
+        if (lane >= d) incl += v;
       }
-      const uint32_t excl = incl - c0 - c1;
-      ftpref[2 * tid] = excl;
-      ftpref[2 * tid + 1] = excl + c0;
-    }
-    __syncthreads();
-
-    const int64_t br = bt / p.nbc, bc = bt % p.nbc;
+      const uint32_t s0 = incl - c0 - c1, s1 = s0 + c0;
+      // row prefix bytes of one FragTile -> H start of each of its 8 rows in [r8][o]
+      auto put = [&](uint32_t ml, uint32_t mh, uint32_t start, uint32_t o) {
+        uint32_t bl = ml - ((ml >> 1) & 0x55555555u);
+        bl = (bl & 0x33333333u) + ((bl >> 2) & 0x33333333u);
+        bl = (bl + (bl >> 4)) & 0x0F0F0F0Fu;
+        uint32_t bh = mh - ((mh >> 1) & 0x55555555u);
+        bh = (bh & 0x33333333u) + ((bh >> 2) & 0x33333333u);
+        bh = (bh + (bh >> 4)) & 0x0F0F0F0Fu;
+        const uint32_t pl = bl * 0x01010100u;                                   // rows 0..3
+        const uint32_t ph = bh * 0x01010100u + ((bl * 0x01010101u) >> 24) * 0x01010101u;  // rows 4..7
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int q = tid + kDecompThreads * i;
-      const int lr = q >> 3, fc = q & 7;        // row in BlockTile, FragTile column
+        for (int r = 0; r < 4; ++r) {
+          hst[r * kHsRow + o] = (uint16_t)(start + ((pl >> (8 * r)) & 0xFFu));
+          hst[(r + 4) * kHsRow + o] = (uint16_t)(start + ((ph >> (8 * r)) & 0xFFu));
+        }
+      };
+      put(m0l, m0h, s0, 2u * lane);
+      put(m1l, m1h, s1, 2u * lane + 1u);
+    }
+    __syncwarp();
+
+    // ---- rows
+    const int64_t br = bt / p.nbc, bc = bt - br * p.nbc;
+    const int64_t col = bc * 64 + fc * 8;
+    const bool full_cols = p.vec_ok && (col + 8 <= p.cols);
+#pragma unroll 4
+    for (int pass = 0; pass < 16; ++pass) {
+      const int lr = 4 * pass + (lane >> 3);                 // row inside the BlockTile
       const int fr = lr >> 3, r8 = lr & 7;
-      const int o = ((fr >> 1) * 4 + (fc >> 1)) * 4 + (fc & 1) * 2 + (fr & 1);  // canonical FT index
-      const uint64_t q1 = P1[o], q2 = P2[o], q3 = P3[o];
-      const uint64_t M = q1 | q2 | q3;
-      const uint32_t hs = ftpref[o] + (uint32_t)__popcll(M & ((1ull << (8 * r8)) - 1ull));
-      const uint32_t ls = (uint32_t)(o * 8 + r8) * 8u - hs;
-      const uint4 v = decode_row(q1, q2, q3, (uint32_t)r8, H, hs, L, ls, lut, p.eb7x2);
+      const uint32_t o = (uint32_t)((fr >> 1) * 16 + (fr & 1)) + ofc;   // canonical FragTile
+      const uint32_t b1 = st[o * 8 + r8];
+      const uint32_t b2 = st[512 + o * 8 + r8];
+      const uint32_t b3 = st[1024 + o * 8 + r8];
+      const uint32_t m = b1 | b2 | b3;
+      const uint32_t hs = hst[r8 * kHsRow + o];
+      const uint32_t ls = (o * 8 + (uint32_t)r8) * 8u - hs;
+      const uint4 v = decode_row_core(b1, b2, b3, m, lut[m], H, hs, L, ls, eb7x2);
       const int64_t row = br * 64 + lr;
-      const int64_t col = bc * 64 + fc * 8;
       if (row < p.rows) {
         uint16_t* dst = p.out + row * p.ld_out + col;
-        if (p.vec_ok && col + 8 <= p.cols) {
+        if (full_cols) {
           *reinterpret_cast<uint4*>(dst) = v;
         } else {
           const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -103,23 +144,25 @@ __global__ void __launch_bounds__(kDecompThreads) decompress_kernel(DecompParams
         }
       }
     }
-    __syncthreads();  // stage s and ftpref are free again
+    __syncwarp();   // stage s and the H-start table are free again
   }
 }
 
-cudaError_t launch_decompress(const DecompParams& p, int grid, size_t smem, cudaStream_t stream) {
+cudaError_t launch_decompress(const DecompParams& p, int grid, int warps, size_t smem, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(decompress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(decompress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  decompress_kernel<<<grid, kDecompThreads, smem, stream>>>(p);
+  decompress_kernel<<<grid, 32 * warps, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
-size_t decompress_smem_bytes(uint32_t stage_bytes) { return 4096 + 256 + 64 + 2 * (size_t)stage_bytes; }
+size_t decompress_smem_bytes(uint32_t stage_bytes, int warps) {
+  return 4096 + 16 * kDecompMaxWarps + kDecompMaxWarps * kHsTabBytes + (size_t)warps * 2 * stage_bytes;
+}
 
-int decompress_threads() { return kDecompThreads; }
+int decompress_max_warps() { return kDecompMaxWarps; }
 
 }  // namespace zs

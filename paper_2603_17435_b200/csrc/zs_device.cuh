@@ -400,7 +400,7 @@ __constant__ uint32_t c_mul[16] = {1u << 28, 128u, 1u << 31, 8u, 1u << 27, 1u <<
                                    ZS_KSPREAD, ZS_KSPREAD << 1, ZS_KSPREAD << 2, ZS_KSPREAD << 4,
                                    ZS_KSPREAD << 5, ZS_KSPREAD << 6, 0u, 0u};
 #ifndef ZS_CMUL
-#define ZS_CMUL 0
+#define ZS_CMUL 1
 #endif
 #if ZS_CMUL
 #define ZS_MUL(idx, imm) c_mul[idx]
@@ -444,7 +444,8 @@ __device__ __forceinline__ uint4 decode_row_abs(uint32_t b1, uint32_t b2, uint32
   const uint32_t h0 = H32[0], h1 = H32[1], h2 = H32[2];
   const uint32_t hlo = __funnelshift_r(h0, h1, hsh8);
   const uint32_t hhi = __funnelshift_r(h1, h2, hsh8);
-  const uint32_t lpair = prmt(Lrow[0], Lrow[1], 0x5410u);   // first two fallback values
+  // first two fallback values (FMA pipe: the ALU pipe is the decoder's bottleneck)
+  const uint32_t lpair = mad_lo(Lrow[1], ZS_MUL(kM16, 1u << 16), Lrow[0]);
 
   uint32_t l1, u1, l2, u2, l3, u3;
   spread_plane<0>(b1, l1, u1);

@@ -41,59 +41,89 @@
 
 namespace zs {
 
-constexpr int kWarpMma = 0;
-constexpr int kWarpProdC = 1;
-constexpr int kWarpProdX = 2;
-constexpr int kWarpAlloc = 3;
-constexpr int kWarpEpi0 = 4;                       // warps 4..7: epilogue (TMEM lane quarters)
-constexpr int kWarpDec0 = 8;                       // warps 8..23: decoders
+// The SMSP arbiter issues from the highest eligible warp id first, so the latency-critical
+// single-warp roles take the TOP ids (a low-id producer / MMA warp starves behind six busy
+// decoder warps on its SMSP and the whole pipeline idles): decoders 0..23, epilogue 24..27.
 constexpr int kDecPerQuarter = 6;
-constexpr int kGemmThreads = 32 * (kWarpDec0 + 4 * kDecPerQuarter);  // 1024
+constexpr int kWarpDec0 = 0;                       // warps 0..23: decoders (lane quarter = warp % 4)
+constexpr int kWarpEpi0 = 4 * kDecPerQuarter;      // warps 24..27: epilogue (TMEM lane quarters)
+constexpr int kWarpAlloc = kWarpEpi0 + 4;          // 28
+constexpr int kWarpProdX = kWarpEpi0 + 5;          // 29
+constexpr int kWarpProdC = kWarpEpi0 + 6;          // 30
+constexpr int kWarpMma = kWarpEpi0 + 7;            // 31
+constexpr int kGemmThreads = 32 * (kWarpEpi0 + 8);  // 1024
 constexpr int kUPS = 4;                            // units per ring stage
-constexpr int kCtrlRegs = 40;                      // setmaxnreg: control/epilogue warps
-constexpr int kDecRegs = 72;                       // setmaxnreg: decoder warps (64K regs total)
 constexpr int kRowBatch = 4;                       // FragTile rows decoded together per thread
-constexpr bool kLutSmem = true;                    // selector table in smem (LDS) vs constant bank (LDC)
 constexpr int kMaxCSlots = 8;
 constexpr int kMaxXSlots = 16;
 constexpr int kMaxASlots = 12;
 constexpr uint32_t kStageMeta = 128;               // see the stage header layout below
 constexpr uint32_t kStagePlanes = 2 * 3 * kUPS * 512;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kRpWarp = 32 * 8 + 32;           // per decoder warp: 32 FragTiles x 8 rows (+ pad)
+constexpr uint32_t kRpWarp = 32 * 16 + 32;          // per decoder warp: 32 FragTiles x 8 rows x u16 (+ pad)
 constexpr uint32_t kRpTabBytes = 4 * kDecPerQuarter * kRpWarp;
 
 // stage header (u32 words): [4i+0..3] unit i {H a, H b, L a, L b} offsets inside the
-// stage regions; [16+q] ticket of lane quarter q; [20+i] unit i has BlockTile row b.
+// stage regions; [20+i] unit i has BlockTile row b; [24] stage index the slot holds.
 
 struct __align__(8) Bars {
   uint64_t full_c[kMaxCSlots];
   uint64_t empty_c[kMaxCSlots];
   uint64_t xfull[kMaxXSlots / kUPS];     // per X-ring stage (4 tiles)
-  uint64_t decoded[kMaxASlots / kUPS];   // per A-ring stage (4 units x 4 quarters x 32 lanes)
-  uint64_t mcommit[2];
+  uint64_t xempty[kMaxXSlots / kUPS];    // X stage consumed (tcgen05.commit after its last unit)
+  uint64_t afree[kMaxASlots];           // TMEM A slot free (tcgen05.commit after the unit's MMAs)
   uint64_t accfull[2];
   uint64_t accempty[2];
   uint32_t tmem_base;
   uint32_t last_flag;
-  uint32_t mma_done;        // # units whose MMAs completed (monotonic)
+  uint32_t tick[4];         // per TMEM lane quarter: next unit to decode (monotonic tickets)
+  uint32_t dcount[kMaxASlots];  // lane quarters decoded into A slot a (monotonic, +4 per unit)
 };
 
 // debug trace: trace[(cta * kTraceUnits + unit) * 16 + event] = clock64, first kTraceCtas CTAs
 constexpr int kTraceCtas = 4, kTraceUnits = 128;
+#ifndef ZS_TRACE
+#define ZS_TRACE 0   // build with -DZS_TRACE=1 for scripts/trace_gemm.py (costs issue slots)
+#endif
 __device__ __forceinline__ void trace_ev(unsigned long long* tr, int unit, int ev) {
+#if ZS_TRACE
+  if (ZS_TRACE == 2 && ev >= 7 && ev < 16 && ev != 6 && (ev < 16) && (threadIdx.x >> 5) < kWarpEpi0) return;
   if (tr != nullptr && blockIdx.x < kTraceCtas && unit < kTraceUnits)
     tr[((size_t)blockIdx.x * kTraceUnits + unit) * 16 + ev] = clock64();
+#else
+  (void)tr; (void)unit; (void)ev;
+#endif
 }
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// x / d for the small ring sizes d (magic = floor(2^32 / d) + 1, exact for x < 2^31 / d)
+__device__ __forceinline__ uint32_t fastdiv(uint32_t x, uint32_t d, uint32_t magic) {
+  return d == 1u ? x : __umulhi(x, magic);
+}
+
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 __device__ __forceinline__ uint32_t bytepop(uint32_t x) {  // popcount of every byte
   x = x - ((x >> 1) & 0x55555555u);
   x = (x & 0x33333333u) + ((x >> 2) & 0x33333333u);
   return (x + (x >> 4)) & 0x0F0F0F0Fu;
+}
+
+__device__ __forceinline__ void wait_count_eq(const uint32_t* ctr, uint32_t want) {
+  uint32_t n = 0;
+  while (ld_acquire_shared(ctr) != want) {
+    __nanosleep(32);
+    if (++n == (1u << 26)) zs_watchdog_fire(ctr, want);
+  }
+}
+
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void wait_count(const uint32_t* ctr, uint32_t need) {
@@ -120,7 +150,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t S_c = p.n_cslots;
   const uint32_t S_x = p.n_xslots;             // multiple of kUPS
   const uint32_t S_a = p.n_aslots;             // multiple of kUPS
-  const uint32_t SXS = S_x / kUPS, SAS = S_a / kUPS;   // stage-granular rings
+  const uint32_t SXS = S_x / kUPS;             // X ring in stages
   const uint32_t capH = p.hcap, capL = p.lcap;
 
   // ---- stream-K range of this CTA (32-bit unit indices; the host checks the range)
@@ -135,19 +165,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   // ---- setup
   if (tid < 256) slut[tid] = c_lut[tid];
+  if (tid < (int)p.n_cslots) reinterpret_cast<uint32_t*>(cslots + (size_t)tid * p.cslot_bytes)[24] = 0xFFFFFFFFu;
   if (tid == 32) {
     for (uint32_t i = 0; i < S_c; ++i) {
       mbar_init(&bars->full_c[i], 1);
-      mbar_init(&bars->empty_c[i], 32 * 4 * kDecPerQuarter);
+      mbar_init(&bars->empty_c[i], 4 * kUPS);   // one arrival per (unit, lane quarter)
     }
-    for (uint32_t i = 0; i < S_x / kUPS; ++i) mbar_init(&bars->xfull[i], 1);
-    for (uint32_t i = 0; i < S_a / kUPS; ++i) mbar_init(&bars->decoded[i], 128 * kUPS);
+    for (uint32_t i = 0; i < S_x / kUPS; ++i) {
+      mbar_init(&bars->xfull[i], 1);
+      mbar_init(&bars->xempty[i], 1);
+    }
+    for (uint32_t i = 0; i < S_a; ++i) {
+      mbar_init(&bars->afree[i], 1);
+      bars->dcount[i] = 0;
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars->mcommit[i], 1);
       mbar_init(&bars->accfull[i], 1);
       mbar_init(&bars->accempty[i], 128);
     }
-    bars->mma_done = 0;
+    for (int i = 0; i < 4; ++i) bars->tick[i] = 0;
     fence_mbar_init();
   }
   if (warp == kWarpAlloc) tmem_alloc<kTmemCols>(&bars->tmem_base);
@@ -220,7 +256,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint32_t* meta = reinterpret_cast<uint32_t*>(cs);
           *reinterpret_cast<uint4*>(meta + 4 * qi) = make_uint4(oha, ohb, ola, olb);
           meta[20 + qi] = has_b ? 1u : 0u;
-          if (qi == 0) *reinterpret_cast<uint4*>(meta + 16) = make_uint4(0, 0, 0, 0);
+          if (qi == 0) meta[24] = (uint32_t)st;   // generation: the stage this slot now holds
         }
         __syncwarp();
         if (mine && qi == 0) {
@@ -256,14 +292,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == kWarpProdX) {
     // ================================================================ activation producer
-    // per stage: the 4 X tiles of its units land on one barrier
+    // per stage: the 4 X tiles of its units land on one barrier; a stage slot is refilled
+    // once the MMA warp's commit after the slot's previous last unit has arrived
     const uint64_t pol = policy_evict_last();
     const uint32_t xbytes = p.n_umma * 128u;
     uint32_t kc = kc0;
-    uint32_t xr = 0;   // X ring stage of st
-    for (int st = 0; st < nstages; ++st, xr = (xr + 1 == SXS) ? 0u : xr + 1u) {
-      // X ring stage xr is free once the MMAs of stage st - SXS have completed
-      wait_count(&bars->mma_done, (st >= (int)SXS) ? (uint32_t)((st - (int)SXS + 1) * kUPS) : 0u);
+    uint32_t xr = 0, xuse = 0;   // X ring stage of st / how often the ring has wrapped
+    for (int st = 0; st < nstages; ++st) {
+      if (xuse > 0) mbar_wait(&bars->xempty[xr], (xuse - 1u) & 1u);
       const int nu = min(kUPS, nunits - st * kUPS);
       if (elect_one()) {
         mbar_arrive_expect_tx(&bars->xfull[xr], xbytes * (uint32_t)nu);
@@ -277,102 +313,96 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       kc += (uint32_t)nu;
       if (kc >= nbc) kc -= nbc;
+      if (++xr == SXS) { xr = 0; ++xuse; }
     }
   } else if (warp == kWarpMma) {
     // ================================================================ MMA issuer
-    // Stage-batched: wait for the stage's X tiles and decoded A slots, issue 4 MMAs per
-    // unit (warp-uniform operands -> uniform registers, ~16 cycles per MMA; see
-    // scripts/umma_probe.cu), commit the stage, then publish the previous stage's
-    // completion as mma_done (monotonic: no mbarrier phase aliasing for the pollers).
+    // Per unit: spin on the A slot's decoded-quarter counter (a plain smem word: one LDS per
+    // probe instead of an mbarrier round trip), issue 4 MMAs (warp-uniform operands ->
+    // uniform registers), commit to the slot's afree barrier (releases the TMEM A slot to
+    // the decoders), to xempty after a stage's last unit and to accfull after a segment's.
+    // No waits on MMA completion in this loop: mbarrier round trips, not the tensor pipe,
+    // limited the per-unit issue rate (~1400 cycles per unit with a commit/poll per unit).
     const uint32_t idesc = umma_idesc_bf16(128, p.n_umma);
     const uint32_t xbase = smem_u32(xslots);
     uint32_t kc = kc0;
     int seg = -1;
-    int pub = 0;   // stages whose completion has been published
-    auto publish = [&]() {
-      ++pub;
-      if (elect_one()) st_release_shared(&bars->mma_done, (uint32_t)min(pub * kUPS, nunits));
-      __syncwarp();
+    // Accumulator hand-off to the epilogue on hardware named barriers 2/3 (sleeping warps
+    // cost no issue slots; a polled mbarrier cost ~17% of all issued instructions).
+    int sig = 0;                                                // segments signalled
+    // segments < seg are fully issued: wake the epilogue for those whose accumulator is done
+    auto try_signal = [&]() {
+      while (sig < seg && mbar_test_wait(&bars->accfull[sig & 1], ((uint32_t)sig >> 1) & 1u)) {
+        named_bar_arrive(2 + (sig & 1), 160);
+        ++sig;
+      }
     };
-    // non-blocking: observe completions of issued stages in order
-    auto poll = [&](int issued) {
-      while (pub < issued && mbar_test_wait(&bars->mcommit[pub & 1], ((uint32_t)pub >> 1) & 1u)) publish();
-    };
-    // ring positions kept incrementally: no integer division on this warp's critical path
-    // (it shares its SM sub-partition with busy decoder warps, so every instruction counts)
-    uint32_t xs = 0, xph = 0, as_ = 0, aph = 0;   // X / A stage ring slot and phase
+    uint32_t xs = 0, xph = 0;                     // X stage ring slot / parity
+    uint32_t as_ = 0, need = 4;                   // A slot ring / decoded count it needs
     uint32_t xa = xbase, ta = tmem_a;             // X tile address / A slot column of the unit
     const uint32_t xa_end = xbase + S_x * p.aslot_bytes, ta_end = tmem_a + 32u * S_a;
-    for (int st = 0; st < nstages; ++st) {
-      // at most two stages in flight (mcommit is a 2-deep ring observed in order)
-      while (pub + 1 < st) {
-        mbar_wait(&bars->mcommit[pub & 1], ((uint32_t)pub >> 1) & 1u);
-        publish();
-      }
-      const int i0 = st * kUPS, i1 = min(nunits, i0 + kUPS);
-      while (!mbar_test_wait(&bars->xfull[xs], xph)) poll(st);
-      while (!mbar_test_wait(&bars->decoded[as_], aph)) poll(st);
-      if (++xs == SXS) { xs = 0; xph ^= 1u; }
-      if (++as_ == SAS) { as_ = 0; aph ^= 1u; }
-      tc_fence_after();
-      // fast path: a full stage strictly inside one accumulation segment -> 16 MMAs from one
-      // set of per-stage operands (the stage's A slots and X tiles are contiguous)
-      if (i1 - i0 == kUPS && i0 != 0 && i1 < nunits && kc != 0 && kc + kUPS < nbc) {
-        const uint32_t d = tmem_base + (uint32_t)(seg & 1) * dcols;
-        const uint64_t bdesc = umma_desc_sw128(xa);
-        const uint32_t bstep = p.aslot_bytes >> 4;   // descriptor address units per X tile
-        if (elect_one()) {
-#pragma unroll
-          for (int i = 0; i < kUPS; ++i) {
-            const uint64_t bd = bdesc + (uint64_t)(bstep * (uint32_t)i);
-            umma_bf16_ts(d, ta + 32u * i, bd, idesc, 1u);
-            umma_bf16_ts(d, ta + 32u * i + 8u, bd + 2, idesc, 1u);
-            umma_bf16_ts(d, ta + 32u * i + 16u, bd + 4, idesc, 1u);
-            umma_bf16_ts(d, ta + 32u * i + 24u, bd + 6, idesc, 1u);
-            trace_ev(p.trace, i0 + i, 6);
-          }
-          umma_commit(&bars->mcommit[st & 1]);
-        }
-        __syncwarp();
-        ta += 32u * kUPS; if (ta == ta_end) ta = tmem_a;
-        xa += kUPS * p.aslot_bytes; if (xa == xa_end) xa = xbase;
-        kc += kUPS;
-        poll(st + 1);
-        continue;
-      }
-      for (int it = i0; it < i1; ++it) {
-        const bool first = (it == 0) || (kc == 0);
-        const bool last = (it == nunits - 1) || (kc + 1 == nbc);
-        if (first) {
-          ++seg;
-          while (!mbar_test_wait(&bars->accempty[seg & 1], (((uint32_t)seg >> 1) & 1u) ^ 1u)) poll(st);
-          tc_fence_after();
-        }
-        const uint32_t d = tmem_base + (uint32_t)(seg & 1) * dcols;
-        const uint32_t at = ta;
-        const uint64_t bdesc = umma_desc_sw128(xa);
-        ta += 32u; if (ta == ta_end) ta = tmem_a;
-        xa += p.aslot_bytes; if (xa == xa_end) xa = xbase;
-        if (elect_one()) {
-          umma_bf16_ts(d, at, bdesc, idesc, first ? 0u : 1u);
-          umma_bf16_ts(d, at + 8u, bdesc + 2, idesc, 1u);
-          umma_bf16_ts(d, at + 16u, bdesc + 4, idesc, 1u);
-          umma_bf16_ts(d, at + 24u, bdesc + 6, idesc, 1u);
-          trace_ev(p.trace, it, 6);
-          if (last) umma_commit(&bars->accfull[seg & 1]);
-        }
-        __syncwarp();
-        if (++kc == nbc) kc = 0;
-      }
-      if (elect_one()) umma_commit(&bars->mcommit[st & 1]);
+    for (int it = 0; it < nunits; ++it) {
+      if (ZS_TRACE == 2 && elect_one()) trace_ev(p.trace, it, 7);
       __syncwarp();
-      poll(st + 1);
+      const bool stage_first = (it & (kUPS - 1)) == 0;
+      const bool stage_last = ((it & (kUPS - 1)) == kUPS - 1) || (it == nunits - 1);
+      if (stage_first) {
+        mbar_wait(&bars->xfull[xs], xph);
+        try_signal();
+      }
+      if (ZS_TRACE == 2 && elect_one()) trace_ev(p.trace, it, 8);
+      __syncwarp();
+      {
+        uint32_t n = 0;
+        while (ld_acquire_shared(&bars->dcount[as_]) < need) {
+          if (++n == (1u << 28)) zs_watchdog_fire(&bars->dcount[as_], need);
+        }
+      }
+      if (ZS_TRACE == 2 && elect_one()) trace_ev(p.trace, it, 9);
+      __syncwarp();
+      tc_fence_after();
+      const bool first = (it == 0) || (kc == 0);
+      const bool last = (it == nunits - 1) || (kc + 1 == nbc);
+      if (first) {
+        ++seg;
+        // the epilogue must have been woken for segment seg - 2 before its buffer is reused
+        while (sig + 1 < seg) {
+          mbar_wait(&bars->accfull[sig & 1], ((uint32_t)sig >> 1) & 1u);
+          named_bar_arrive(2 + (sig & 1), 160);
+          ++sig;
+        }
+        mbar_wait(&bars->accempty[seg & 1], (((uint32_t)seg >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+      }
+      const uint32_t d = tmem_base + (uint32_t)(seg & 1) * dcols;
+      const uint64_t bdesc = umma_desc_sw128(xa);
+      if (elect_one()) {
+        if (!(p.dbg & 4)) {
+          umma_bf16_ts(d, ta, bdesc, idesc, first ? 0u : 1u);
+          umma_bf16_ts(d, ta + 8u, bdesc + 2, idesc, 1u);
+          umma_bf16_ts(d, ta + 16u, bdesc + 4, idesc, 1u);
+          umma_bf16_ts(d, ta + 24u, bdesc + 6, idesc, 1u);
+        }
+        trace_ev(p.trace, it, 6);
+        umma_commit(&bars->afree[as_]);
+        if (stage_last) umma_commit(&bars->xempty[xs]);
+        if (last) umma_commit(&bars->accfull[seg & 1]);
+        if (ZS_TRACE == 2) trace_ev(p.trace, it, 10);
+      }
+      __syncwarp();
+      ta += 32u; if (ta == ta_end) ta = tmem_a;
+      xa += p.aslot_bytes; if (xa == xa_end) xa = xbase;
+      if (++as_ == S_a) { as_ = 0; need += 4; }
+      if (stage_last) { if (++xs == SXS) { xs = 0; xph ^= 1u; } }
+      if (++kc == nbc) kc = 0;
     }
-    while (pub < nstages) {
-      mbar_wait(&bars->mcommit[pub & 1], ((uint32_t)pub >> 1) & 1u);
-      publish();
+    // the last segment(s): wait for their accumulators, then wake the epilogue
+    while (sig <= seg) {
+      mbar_wait(&bars->accfull[sig & 1], ((uint32_t)sig >> 1) & 1u);
+      named_bar_arrive(2 + (sig & 1), 160);
+      ++sig;
     }
-  } else if (warp >= kWarpDec0) {
+  } else if (warp < kWarpEpi0) {
     // ================================================================ decoders
     const int q = warp & 3;                       // TMEM lane quarter (== warp % 4)
     const int bt_sel = q >> 1, hh = q & 1;
@@ -380,42 +410,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int fr = lr >> 3, r8 = lr & 7;
     const int tr = fr >> 1;                       // TensorCoreTile row of this thread's FragTiles
     const uint32_t obase = (uint32_t)(tr * 16 + (fr & 1));                 // o for fc = 0
-    const int srcbase = (tr - 2 * hh) * 16 + (fr & 1);
     const uint32_t tq = tmem_a + ((uint32_t)(32 * q) << 16);
     const int fo = 32 * hh + lane;                // scan lane's FragTile
     // row-prefix table of this warp: FragTile o (local 0..31) at o*8 + (o >> 4)*16 (the pad
     // keeps the 4 FragTiles a warp reads at once on distinct banks)
     uint8_t* rpt = rptab + (warp - kWarpDec0) * kRpWarp;
-    const uint32_t rp_wr = (uint32_t)lane * 8u + ((uint32_t)lane >> 4) * 16u;
+    // row table: FragTile o (local 0..31) at o*16 + (o >> 4)*32 bytes, row r8 at + 2*r8 (the
+    // pad keeps the 4 FragTiles a warp reads at once on distinct banks)
+    const uint32_t rp_wr = (uint32_t)lane * 16u + ((uint32_t)lane >> 4) * 32u;
     const uint32_t ol0 = obase - 32u * hh;        // local FragTile index for fc = 0
-    // The decoded-barrier arrival of a unit is deferred until after the next unit's scan,
-    // so the tcgen05.st completion wait overlaps useful work.
-    int pend = -1;                                // A-ring stage of the pending arrival, -1 = none
-    auto flush = [&]() {
-      if (pend >= 0) {
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&bars->decoded[pend]);
-        pend = -1;
-      }
-    };
-    uint32_t slot = 0, cph = 0, astg = 0;         // C ring slot / phase, A ring stage (no divisions)
-    for (int st = 0; st < nstages; ++st, slot = (slot + 1 == S_c) ? 0u : slot + 1u, cph ^= (slot == 0),
-             astg = (astg + 1 == SAS) ? 0u : astg + 1u) {
-      mbar_wait(&bars->full_c[slot], cph);
+    // Tickets: the warps of a quarter take units from one monotonic counter, so no warp idles
+    // while a loaded unit is waiting (a stage holds kUPS units, 4 x kUPS unit-quarters).
+    while (true) {
+      uint32_t u = 0;
+      if (lane == 0) u = atomicAdd(&bars->tick[q], 1u);
+      u = shfl_idx(u, 0);
+      if ((int)u >= nunits) break;
+      if (lane == 0 && q < 2) trace_ev(p.trace, (int)u, q == 0 ? 1 : 15);   // ticket drawn
+      const int st = (int)(u / kUPS);
+      const uint32_t j = u % kUPS;
+      const uint32_t stc = fastdiv((uint32_t)st, S_c, p.cdiv_magic);
+      const uint32_t slot = (uint32_t)st - stc * S_c, cph = stc & 1u;
+      const uint32_t ag = fastdiv(u, S_a, p.adiv_magic);            // use count of the slot
+      const uint32_t a = u - ag * S_a;                               // TMEM A slot of this unit
       const uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
       const uint32_t* meta = reinterpret_cast<const uint32_t*>(cs);
-      uint32_t* tickets = const_cast<uint32_t*>(meta) + 16;
-      const int nu = min(kUPS, nunits - st * kUPS);
-      while (true) {   // 4 tickets per quarter and stage (tickets >= nu only arrive)
-        uint32_t j = 0;
-        if (lane == 0) j = atomicAdd(&tickets[q], 1u);
-        j = shfl_idx(j, 0);
-        if ((int)j >= kUPS) break;
-        const int it = st * kUPS + (int)j;
-        const uint32_t a = astg * kUPS + j;   // A slot of this unit
-        const bool present = ((int)j < nu) && ((bt_sel == 0) || (meta[20 + j] != 0u));
-        if (lane == 0 && (int)j < nu) trace_ev(p.trace, it, 7 + q);
+      // The slot's header names the stage it holds (meta[24]); once it names st, the parity
+      // wait below cannot alias an older fill.
+      if (ld_acquire_shared(meta + 24) != (uint32_t)st || !mbar_test_wait(&bars->full_c[slot], cph)) {
+        wait_count_eq(meta + 24, (uint32_t)st);
+        mbar_wait(&bars->full_c[slot], cph);
+      }
+      {
+        const int it = (int)u;
+        const bool present = (bt_sel == 0) || (meta[20 + j] != 0u);
+        if (lane == 0) trace_ev(p.trace, it, 7 + q);
         if (present) {
           const uint4 mt = *reinterpret_cast<const uint4*>(meta + 4 * j);  // {H a, H b, L a, L b}
           const uint8_t* P1 = cs + kStageMeta + (bt_sel * 3) * (kUPS * 512) + j * 512;
@@ -444,16 +473,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint2 t3 = *reinterpret_cast<const uint2*>(P3 + lane * 8);
             excl += __reduce_add_sync(0xFFFFFFFFu, __popc(t1.x | t2.x | t3.x) + __popc(t1.y | t2.y | t3.y));
           }
-          // exclusive per-row prefix inside the FragTile, one byte per row
+          // H start of each of the FragTile's 8 rows (relative to the unit's H base), u16
           const uint32_t bl = bytepop(mlo), bh = bytepop(mhi);
           const uint32_t rp_lo = bl * 0x01010100u;
           const uint32_t rp_hi = bh * 0x01010100u + ((bl * 0x01010101u) >> 24) * 0x01010101u;
+          const uint32_t ex2 = excl * 0x10001u;
+          const uint4 hrow = make_uint4(prmt(rp_lo, 0u, 0x4140u) + ex2, prmt(rp_lo, 0u, 0x4342u) + ex2,
+                                        prmt(rp_hi, 0u, 0x4140u) + ex2, prmt(rp_hi, 0u, 0x4342u) + ex2);
           __syncwarp();   // previous unit's readers are done
-          *reinterpret_cast<uint2*>(rpt + rp_wr) = make_uint2(rp_lo, rp_hi);
+          *reinterpret_cast<uint4*>(rpt + rp_wr) = hrow;
           __syncwarp();
-          flush();
-          // A slot a must be free: the MMAs of stage st - SAS have completed
-          wait_count(&bars->mma_done, (st >= (int)SAS) ? (uint32_t)((st - (int)SAS + 1) * kUPS) : 0u);
+          // the slot is free once the MMAs of unit u - S_a have completed (their commit)
+          if (ag > 0) mbar_wait(&bars->afree[a], (ag - 1u) & 1u);
           tc_fence_after();
           if (lane == 0) trace_ev(p.trace, it, 11 + q);
           const uint32_t taddr0 = tq + 32u * a;
@@ -461,19 +492,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // per-unit base plus an immediate.  FragTile of row f: o = obase + cf(f),
           // cf(f) = (f>>1)*4 + (f&1)*2 (canonical order of FragTile column f).
           const uint32_t hb = (uint32_t)(H - smem);                     // 16-B aligned
-          const uint32_t pexcl = excl + hb;                             // FragTile H start, absolute
           const uint8_t* pb = P1 + obase * 8u + (uint32_t)r8;           // this row's plane byte, f = 0
-          const uint8_t* rb = rpt + ol0 * 8u + (ol0 >> 4) * 16u + (uint32_t)r8;
+          const uint8_t* rb = rpt + ol0 * 16u + (ol0 >> 4) * 32u + 2u * (uint32_t)r8;
           const uint32_t la0 = (uint32_t)((const uint8_t*)L - smem) + 2u * hb +
                                16u * (obase * 8u + (uint32_t)r8);      // + 128 cf(f) - 2 hs_abs
 #pragma unroll
           for (int fb = 0; fb < 8; fb += kRowBatch) {
+            if (p.dbg & 1) break;
             uint4 v[kRowBatch];
 #pragma unroll
             for (int qq = 0; qq < kRowBatch; ++qq) {
               const int f = fb + qq;
               const uint32_t cf = (uint32_t)((f >> 1) * 4 + (f & 1) * 2);
-              const uint32_t hs_abs = shfl_idx(pexcl, srcbase + (int)cf) + rb[cf * 8u];
+              const uint32_t hs_abs = hb + *reinterpret_cast<const uint16_t*>(rb + cf * 16u);
               const uint32_t b1 = pb[cf * 8u];
               const uint32_t b2 = pb[cf * 8u + kUPS * 512];
               const uint32_t b3 = pb[cf * 8u + 2 * kUPS * 512];
@@ -483,21 +514,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                      reinterpret_cast<const uint16_t*>(smem + mad_lo(hs_abs, ZS_MUL(kMNeg2, 0xFFFFFFFEu), la0 + 128u * cf)),
                                      p.eb7x2);
             }
+            if (p.dbg & 2) {
+              uint32_t x = 0;
 #pragma unroll
-            for (int qq = 0; qq < kRowBatch; qq += 2) tmem_st8(taddr0 + 4u * (fb + qq), v[qq], v[qq + 1]);
+              for (int qq = 0; qq < kRowBatch; ++qq) x ^= v[qq].x ^ v[qq].y ^ v[qq].z ^ v[qq].w;
+              if (x == 0x9E3779B9u) p.counters[0] = x;   // keeps the decode live
+            } else {
+#pragma unroll
+              for (int qq = 0; qq < kRowBatch; qq += 2) tmem_st8(taddr0 + 4u * (fb + qq), v[qq], v[qq + 1]);
+            }
           }
-          pend = (int)astg;
-          if (lane == 0) trace_ev(p.trace, it, 2 + q);
-        } else {
-          flush();
+          // publish the unit-quarter at once (the MMA warp spins on the slot's counter)
+          tmem_wait_st();
           tc_fence_before();
-          mbar_arrive(&bars->decoded[astg]);
+          __syncwarp();
+          if (lane == 0) red_release_add(&bars->dcount[a], 1u);
+          if (lane == 0) trace_ev(p.trace, it, 2 + q);
+        } else {   // absent BlockTile row b (odd row count): nothing to decode
+          if (ag > 0) mbar_wait(&bars->afree[a], (ag - 1u) & 1u);
+          if (lane == 0) red_release_add(&bars->dcount[a], 1u);
         }
       }
-      mbar_arrive(&bars->empty_c[slot]);   // this warp no longer reads the stage's smem
+      __syncwarp();                                    // all lanes done reading the stage
+      if (lane == 0) mbar_arrive(&bars->empty_c[slot]);
     }
-    flush();
-  } else if (warp >= kWarpEpi0) {
+  } else if (warp < kWarpEpi0 + 4) {
     // ================================================================ epilogue (warps 4..7)
     const int et = tid - 32 * kWarpEpi0;  // 0..127 = TMEM lane = row inside the band
     const int eq = warp & 3;              // TMEM lane quarter
@@ -506,7 +547,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (uint32_t band = band0; band <= b_last; ++band, ++seg) {
       const uint32_t s0 = max(u0, band * nbc), s1 = min(u1, (band + 1) * nbc);
       const bool full = (s1 - s0) == nbc;
-      mbar_wait_sleep(&bars->accfull[seg & 1], ((uint32_t)seg >> 1) & 1u);
+      // sleep on the named barrier the MMA warp arrives at once the segment's MMAs are
+      // complete; the mbarrier wait after it then passes at once (and orders the TMEM reads)
+      named_bar_sync(2 + (seg & 1), 160);
+      mbar_wait(&bars->accfull[seg & 1], ((uint32_t)seg >> 1) & 1u);
       tc_fence_after();
       const int64_t n = (int64_t)band * 128 + et;
       const bool nvalid = n < p.N;
@@ -541,11 +585,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (bars->last_flag) {
           __threadfence();
           if (nvalid) {
-            for (int m = 0; m < p.mc; ++m) {
-              float* wp = p.ws + (int64_t)m * p.N + n;
-              const float f = __ldcg(wp);
-              p.y[(int64_t)(p.m0 + m) * p.ldy + n] = __bfloat16_as_ushort(__float2bfloat16_rn(f));
-              __stcg(wp, 0.0f);
+            // 16 independent loads in flight per batch (a rolled loop serialises one L2
+            // round trip per token: ~13 us at M = 32 on the kernel's critical tail)
+            for (int m0 = 0; m0 < p.mc; m0 += 16) {
+              float f[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                f[j] = (m0 + j < p.mc) ? __ldcg(p.ws + (int64_t)(m0 + j) * p.N + n) : 0.0f;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                if (m0 + j < p.mc) {
+                  p.y[(int64_t)(p.m0 + m0 + j) * p.ldy + n] = __bfloat16_as_ushort(__float2bfloat16_rn(f[j]));
+                  __stcg(p.ws + (int64_t)(m0 + j) * p.N + n, 0.0f);
+                }
+              }
             }
           }
           if (et == 0) p.counters[band] = 0u;

@@ -24,9 +24,9 @@ struct DecompParams {
   int vec_ok;
 };
 
-cudaError_t launch_decompress(const DecompParams& p, int grid, size_t smem, cudaStream_t stream);
-size_t decompress_smem_bytes(uint32_t stage_bytes);
-int decompress_threads();
+cudaError_t launch_decompress(const DecompParams& p, int grid, int warps, size_t smem, cudaStream_t stream);
+size_t decompress_smem_bytes(uint32_t stage_bytes, int warps);
+int decompress_max_warps();
 
 struct GemmParams {
   const uint64_t* b1;
@@ -53,7 +53,9 @@ struct GemmParams {
   uint32_t n_aslots;        // TMEM A-operand ring (32 columns each, multiple of 4)
   uint32_t acc_cols;        // TMEM columns per accumulator buffer (>= n_umma, multiple of 32)
   uint32_t eb7x2;
+  uint32_t cdiv_magic, adiv_magic;  // fastdiv multipliers of n_cslots / n_aslots
   unsigned long long* trace;  // optional per-unit event timestamps (debug; nullptr = off)
+  uint32_t dbg;               // debug experiment flags (0 in production; zs_debug_set_flags)
 };
 
 cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, size_t smem, cudaStream_t stream);

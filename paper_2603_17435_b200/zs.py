@@ -13,14 +13,14 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libzs.so")
+LIB_PATH = os.environ.get("ZS_LIB") or os.path.join(_PKG, "libzs.so")   # ZS_LIB: debug builds
 
 ZS_STATUS = {0: "ZS_OK", 1: "ZS_ERR_INVALID_ARG", 2: "ZS_ERR_SHAPE", 3: "ZS_ERR_ALIGNMENT",
              4: "ZS_ERR_UNSUPPORTED", 5: "ZS_ERR_CORRUPT", 6: "ZS_ERR_CUDA", 7: "ZS_ERR_CAPACITY"}
 
 # every symbol include/zs.h declares (checked by tests/test_abi.py)
 EXPORTS = ["zs_encode_bound", "zs_encode_measure", "zs_encode", "zs_decompress", "zs_gemm_workspace_bytes",
-           "zs_gemm", "zs_last_launch_count", "zs_status_string"]
+           "zs_gemm_is_decoupled", "zs_gemm", "zs_last_launch_count", "zs_status_string"]
 
 
 class ZsError(RuntimeError):
@@ -61,6 +61,8 @@ def lib():
         L.zs_decompress.argtypes = [ctypes.POINTER(zs_tensor), vp, i64, vp]
         L.zs_gemm_workspace_bytes.argtypes = [i64, i64, i64]
         L.zs_gemm_workspace_bytes.restype = ctypes.c_size_t
+        L.zs_gemm_is_decoupled.argtypes = [i64]
+        L.zs_gemm_is_decoupled.restype = ctypes.c_int
         L.zs_gemm.argtypes = [vp, i64, ctypes.POINTER(zs_tensor), vp, i64, i64, i64, i64, vp, ctypes.c_size_t, vp]
         L.zs_status_string.argtypes = [ctypes.c_int]
         L.zs_status_string.restype = ctypes.c_char_p
@@ -223,10 +225,12 @@ _WS = {}
 
 
 def workspace(M: int, N: int, K: int, device):
-    """Zero-initialised, self-cleaning split-K workspace (kept per device, grown on demand)."""
+    """zs_gemm workspace, kept per device and grown on demand: the zero-initialised,
+    self-cleaning split-K buffer of the fused path, or the decoded-weight scratch of the
+    decoupled (large-M) path -- two separate buffers, since the latter is left dirty."""
     import torch
     need = int(lib().zs_gemm_workspace_bytes(M, N, K))
-    key = str(device)
+    key = (str(device), int(lib().zs_gemm_is_decoupled(M)))
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
         ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)

@@ -1,4 +1,10 @@
-"""Per-unit pipeline timeline of zipgemm_kernel (debug hook zs_debug_set_trace)."""
+"""Per-unit pipeline timeline of zipgemm_kernel (debug hook zs_debug_set_trace).
+
+Needs the trace build:  python -m paper_2603_17435_b200.build --trace
+                        ZS_LIB=paper_2603_17435_b200/libzs_trace.so python scripts/trace_gemm.py L M [flags]
+Events: prod = stage issued, tick0/tick1 = ticket drawn (quarter 0/1), drN = stage data ready,
+asN = A slot free, dqN = unit-quarter decoded, mma = MMAs issued.
+"""
 import ctypes
 import os
 import sys
@@ -22,15 +28,16 @@ L = Z.lib()
 L.zs_debug_set_trace.argtypes = [ctypes.c_void_p]
 L.zs_debug_set_ring.argtypes = [ctypes.c_int]
 if len(sys.argv) > 3:
-    L.zs_debug_set_ring(int(sys.argv[3]))
+    L.zs_debug_set_flags.argtypes = [ctypes.c_int]
+    L.zs_debug_set_flags(int(sys.argv[3]))
 for _ in range(3):
     Z.gemm(x, wd)
 L.zs_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
 Z.gemm(x, wd)
 torch.cuda.synchronize()
 L.zs_debug_set_trace(None)
-t = tr.cpu().numpy().reshape(4, 128, 16).astype(np.int64)[:, :, :15]
-names = ["prod", "-", "dq0", "dq1", "dq2", "dq3", "mma", "tk0", "tk1", "tk2", "tk3", "as0", "as1", "as2", "as3"]
+t = tr.cpu().numpy().reshape(4, 128, 16).astype(np.int64)[:, :, :16]
+names = ["prod", "tick0", "dq0", "dq1", "dq2", "dq3", "mma", "dr0", "dr1", "dr2", "dr3", "as0", "as1", "as2", "as3", "tick1"]
 # summary over the first 4 CTAs: decode duration (slot-acquired -> done) and ticket->done
 d1, d2 = [], []
 for cta in range(4):
@@ -41,8 +48,10 @@ for cta in range(4):
                 d1.append(r[2 + q] - r[11 + q])
             if r[2 + q] and r[7 + q]:
                 d2.append(r[2 + q] - r[7 + q])
-print("decode (A slot ready -> done) cycles: mean %.0f  p10 %.0f  p90 %.0f" % (np.mean(d1), np.percentile(d1, 10), np.percentile(d1, 90)))
-print("ticket -> done cycles: mean %.0f" % np.mean(d2))
+if d1:
+    print("decode (A slot ready -> done) cycles: mean %.0f  p10 %.0f  p90 %.0f" % (np.mean(d1), np.percentile(d1, 10), np.percentile(d1, 90)))
+if d2:
+    print("ticket -> done cycles: mean %.0f" % np.mean(d2))
 for cta in range(4):
     r = t[cta]
     nz = r[r > 0]
@@ -54,7 +63,7 @@ for cta in range(1):
     base = t[cta][t[cta] > 0].min()
     print(f"CTA {cta}: times in cycles relative to first event")
     print("unit " + " ".join(f"{n:>8s}" for n in names))
-    for u in range(0, 24):
+    for u in range(0, 100):
         row = t[cta, u]
         if row.max() == 0:
             break

@@ -92,10 +92,10 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 16);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
-  for (int stw : {0, 8, 16, 24})
-  for (int ts = 1; ts < 2; ++ts)
-    for (uint32_t N : {32u})
-      for (int nacc : {8})
+  for (int stw : {0, 24})
+  for (int ts = 0; ts < 2; ++ts)
+    for (uint32_t N : {16u, 32u, 64u, 256u})
+      for (int nacc : {1})
       for (int n : {512}) {
         printf("st_warps=%d ", stw);
         probe<<<1, 128 + 32 * (stw + 4), 70 * 1024>>>(n, N, ts, nacc, d, stw);
