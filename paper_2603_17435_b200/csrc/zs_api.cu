@@ -279,7 +279,7 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
     p.n_aslots = na - na % 4;
     auto magic = [](uint32_t d) { return d <= 1u ? 0u : (uint32_t)((1ull << 32) / d + 1ull); };
     p.cdiv_magic = magic(p.n_cslots);
-    p.adiv_magic = magic(p.n_aslots);
+    p.adiv_magic = magic(p.n_aslots / 4);
     if (p.n_umma != cur_box) {
       cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
       cuuint64_t strides[1] = {(cuuint64_t)(ldx * 2)};

@@ -71,13 +71,13 @@ struct __align__(8) Bars {
   uint64_t empty_c[kMaxCSlots];
   uint64_t xfull[kMaxXSlots / kUPS];     // per X-ring stage (4 tiles)
   uint64_t xempty[kMaxXSlots / kUPS];    // X stage consumed (tcgen05.commit after its last unit)
-  uint64_t afree[kMaxASlots];           // TMEM A slot free (tcgen05.commit after the unit's MMAs)
+  uint64_t afree[kMaxASlots / kUPS];    // TMEM A stage free (tcgen05.commit after its MMAs)
   uint64_t accfull[2];
   uint64_t accempty[2];
   uint32_t tmem_base;
   uint32_t last_flag;
   uint32_t tick[4];         // per TMEM lane quarter: next unit to decode (monotonic tickets)
-  uint32_t dcount[kMaxASlots];  // lane quarters decoded into A slot a (monotonic, +4 per unit)
+  alignas(16) uint32_t dcount[kMaxASlots];  // lane quarters decoded into A slot a (monotonic, +4 per use)
 };
 
 // debug trace: trace[(cta * kTraceUnits + unit) * 16 + event] = clock64, first kTraceCtas CTAs
@@ -175,10 +175,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&bars->xfull[i], 1);
       mbar_init(&bars->xempty[i], 1);
     }
-    for (uint32_t i = 0; i < S_a; ++i) {
-      mbar_init(&bars->afree[i], 1);
-      bars->dcount[i] = 0;
-    }
+    for (uint32_t i = 0; i < S_a; ++i) bars->dcount[i] = 0;
+    for (uint32_t i = 0; i < S_a / kUPS; ++i) mbar_init(&bars->afree[i], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->accfull[i], 1);
       mbar_init(&bars->accempty[i], 128);
@@ -317,14 +315,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == kWarpMma) {
     // ================================================================ MMA issuer
-    // Per unit: spin on the A slot's decoded-quarter counter (a plain smem word: one LDS per
-    // probe instead of an mbarrier round trip), issue 4 MMAs (warp-uniform operands ->
-    // uniform registers), commit to the slot's afree barrier (releases the TMEM A slot to
-    // the decoders), to xempty after a stage's last unit and to accfull after a segment's.
-    // No waits on MMA completion in this loop: mbarrier round trips, not the tensor pipe,
-    // limited the per-unit issue rate (~1400 cycles per unit with a commit/poll per unit).
+    // Stage-batched (4 units per iteration): this single warp shares its SMSP with six busy
+    // decoder warps and is issued round-robin with them, so every instruction of its loop
+    // costs ~7 cycles; a per-unit loop of waits / fences / commits took ~1000 cycles per
+    // unit.  Readiness is a plain smem counter per A slot (decoded lane quarters); one
+    // commit per stage frees the stage's TMEM A slots and X tiles.
     const uint32_t idesc = umma_idesc_bf16(128, p.n_umma);
     const uint32_t xbase = smem_u32(xslots);
+    const uint32_t SAS = S_a / kUPS;
     uint32_t kc = kc0;
     int seg = -1;
     // Accumulator hand-off to the epilogue on hardware named barriers 2/3 (sleeping warps
@@ -338,63 +336,86 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     };
     uint32_t xs = 0, xph = 0;                     // X stage ring slot / parity
-    uint32_t as_ = 0, need = 4;                   // A slot ring / decoded count it needs
-    uint32_t xa = xbase, ta = tmem_a;             // X tile address / A slot column of the unit
+    uint32_t as_ = 0, need = 4;                   // A stage ring / decoded count each slot needs
+    uint32_t xa = xbase, ta = tmem_a;             // X tile address / A slot column of the stage
     const uint32_t xa_end = xbase + S_x * p.aslot_bytes, ta_end = tmem_a + 32u * S_a;
-    for (int it = 0; it < nunits; ++it) {
-      if (ZS_TRACE == 2 && elect_one()) trace_ev(p.trace, it, 7);
-      __syncwarp();
-      const bool stage_first = (it & (kUPS - 1)) == 0;
-      const bool stage_last = ((it & (kUPS - 1)) == kUPS - 1) || (it == nunits - 1);
-      if (stage_first) {
-        mbar_wait(&bars->xfull[xs], xph);
-        try_signal();
-      }
-      if (ZS_TRACE == 2 && elect_one()) trace_ev(p.trace, it, 8);
-      __syncwarp();
-      {
+    for (int st = 0; st < nstages; ++st) {
+      const int i0 = st * kUPS, nu = min(kUPS, nunits - i0);
+      mbar_wait(&bars->xfull[xs], xph);
+      try_signal();
+      for (int j = 0; j < nu; ++j) {
+        const uint32_t* c = &bars->dcount[as_ * kUPS + j];
         uint32_t n = 0;
-        while (ld_acquire_shared(&bars->dcount[as_]) < need) {
-          if (++n == (1u << 28)) zs_watchdog_fire(&bars->dcount[as_], need);
+        while (ld_acquire_shared(c) < need) {
+          if (++n == (1u << 28)) zs_watchdog_fire(c, need);
         }
       }
-      if (ZS_TRACE == 2 && elect_one()) trace_ev(p.trace, it, 9);
-      __syncwarp();
       tc_fence_after();
-      const bool first = (it == 0) || (kc == 0);
-      const bool last = (it == nunits - 1) || (kc + 1 == nbc);
-      if (first) {
-        ++seg;
-        // the epilogue must have been woken for segment seg - 2 before its buffer is reused
-        while (sig + 1 < seg) {
-          mbar_wait(&bars->accfull[sig & 1], ((uint32_t)sig >> 1) & 1u);
-          named_bar_arrive(2 + (sig & 1), 160);
-          ++sig;
+      if (nu == kUPS && i0 != 0 && i0 + kUPS < nunits && kc != 0 && kc + kUPS < nbc) {
+        // fast path: a full stage strictly inside one accumulation segment -> 16 MMAs from
+        // one set of per-stage operands (the stage's A slots and X tiles are contiguous)
+        const uint32_t d = tmem_base + (uint32_t)(seg & 1) * dcols;
+        const uint64_t bdesc = umma_desc_sw128(xa);
+        const uint32_t bstep = p.aslot_bytes >> 4;   // descriptor address units per X tile
+        if (elect_one()) {
+          if (!(p.dbg & 4)) {
+#pragma unroll
+            for (int i = 0; i < kUPS; ++i) {
+              const uint64_t bd = bdesc + (uint64_t)(bstep * (uint32_t)i);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) umma_bf16_ts(d, ta + 32u * i + 8u * k, bd + 2 * k, idesc, 1u);
+            }
+          }
+          umma_commit(&bars->afree[as_]);
+          umma_commit(&bars->xempty[xs]);
         }
-        mbar_wait(&bars->accempty[seg & 1], (((uint32_t)seg >> 1) & 1u) ^ 1u);
-        tc_fence_after();
-      }
-      const uint32_t d = tmem_base + (uint32_t)(seg & 1) * dcols;
-      const uint64_t bdesc = umma_desc_sw128(xa);
-      if (elect_one()) {
-        if (!(p.dbg & 4)) {
-          umma_bf16_ts(d, ta, bdesc, idesc, first ? 0u : 1u);
-          umma_bf16_ts(d, ta + 8u, bdesc + 2, idesc, 1u);
-          umma_bf16_ts(d, ta + 16u, bdesc + 4, idesc, 1u);
-          umma_bf16_ts(d, ta + 24u, bdesc + 6, idesc, 1u);
+        __syncwarp();
+        ta += 32u * kUPS; if (ta == ta_end) ta = tmem_a;
+        xa += kUPS * p.aslot_bytes; if (xa == xa_end) xa = xbase;
+        kc += kUPS;
+      } else {
+        for (int j = 0; j < nu; ++j) {
+          const int it = i0 + j;
+          const bool first = (it == 0) || (kc == 0);
+          const bool last = (it == nunits - 1) || (kc + 1 == nbc);
+          if (first) {
+            ++seg;
+            // the epilogue must have been woken for segment seg - 2 before its buffer is reused
+            while (sig + 1 < seg) {
+              mbar_wait(&bars->accfull[sig & 1], ((uint32_t)sig >> 1) & 1u);
+              named_bar_arrive(2 + (sig & 1), 160);
+              ++sig;
+            }
+            mbar_wait(&bars->accempty[seg & 1], (((uint32_t)seg >> 1) & 1u) ^ 1u);
+            tc_fence_after();
+          }
+          const uint32_t d = tmem_base + (uint32_t)(seg & 1) * dcols;
+          const uint64_t bdesc = umma_desc_sw128(xa);
+          if (elect_one()) {
+            if (!(p.dbg & 4)) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                umma_bf16_ts(d, ta + 8u * k, bdesc + 2 * k, idesc, (first && k == 0) ? 0u : 1u);
+            }
+            trace_ev(p.trace, it, 6);
+            if (last) umma_commit(&bars->accfull[seg & 1]);
+            if (j == nu - 1) {
+              umma_commit(&bars->afree[as_]);
+              umma_commit(&bars->xempty[xs]);
+            }
+          }
+          __syncwarp();
+          ta += 32u; if (ta == ta_end) ta = tmem_a;
+          xa += p.aslot_bytes; if (xa == xa_end) xa = xbase;
+          if (++kc == nbc) kc = 0;
         }
-        trace_ev(p.trace, it, 6);
-        umma_commit(&bars->afree[as_]);
-        if (stage_last) umma_commit(&bars->xempty[xs]);
-        if (last) umma_commit(&bars->accfull[seg & 1]);
-        if (ZS_TRACE == 2) trace_ev(p.trace, it, 10);
+        // a partial last stage leaves its remaining A slots unused: skip them
+        if (nu < kUPS) {
+          ta += 32u * (uint32_t)(kUPS - nu); if (ta >= ta_end) ta -= ta_end - tmem_a;
+        }
       }
-      __syncwarp();
-      ta += 32u; if (ta == ta_end) ta = tmem_a;
-      xa += p.aslot_bytes; if (xa == xa_end) xa = xbase;
-      if (++as_ == S_a) { as_ = 0; need += 4; }
-      if (stage_last) { if (++xs == SXS) { xs = 0; xph ^= 1u; } }
-      if (++kc == nbc) kc = 0;
+      if (++as_ == SAS) { as_ = 0; need += 4; }
+      if (++xs == SXS) { xs = 0; xph ^= 1u; }
     }
     // the last segment(s): wait for their accumulators, then wake the epilogue
     while (sig <= seg) {
@@ -431,8 +452,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t j = u % kUPS;
       const uint32_t stc = fastdiv((uint32_t)st, S_c, p.cdiv_magic);
       const uint32_t slot = (uint32_t)st - stc * S_c, cph = stc & 1u;
-      const uint32_t ag = fastdiv(u, S_a, p.adiv_magic);            // use count of the slot
-      const uint32_t a = u - ag * S_a;                               // TMEM A slot of this unit
+      const uint32_t SAS = S_a / kUPS;
+      const uint32_t ag = fastdiv((uint32_t)st, SAS, p.adiv_magic);  // use count of the A stage
+      const uint32_t astg = (uint32_t)st - ag * SAS;                 // TMEM A stage of this unit
+      const uint32_t a = astg * kUPS + j;                            // TMEM A slot of this unit
       const uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
       const uint32_t* meta = reinterpret_cast<const uint32_t*>(cs);
       // The slot's header names the stage it holds (meta[24]); once it names st, the parity
@@ -483,8 +506,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           __syncwarp();   // previous unit's readers are done
           *reinterpret_cast<uint4*>(rpt + rp_wr) = hrow;
           __syncwarp();
-          // the slot is free once the MMAs of unit u - S_a have completed (their commit)
-          if (ag > 0) mbar_wait(&bars->afree[a], (ag - 1u) & 1u);
+          // the slot is free once the MMAs of stage st - SAS have completed (their commit)
+          if (ag > 0) mbar_wait(&bars->afree[astg], (ag - 1u) & 1u);
           tc_fence_after();
           if (lane == 0) trace_ev(p.trace, it, 11 + q);
           const uint32_t taddr0 = tq + 32u * a;
@@ -531,7 +554,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (lane == 0) red_release_add(&bars->dcount[a], 1u);
           if (lane == 0) trace_ev(p.trace, it, 2 + q);
         } else {   // absent BlockTile row b (odd row count): nothing to decode
-          if (ag > 0) mbar_wait(&bars->afree[a], (ag - 1u) & 1u);
+          if (ag > 0) mbar_wait(&bars->afree[astg], (ag - 1u) & 1u);
           if (lane == 0) red_release_add(&bars->dcount[a], 1u);
         }
       }
