@@ -124,3 +124,22 @@ def test_validation_errors_without_gpu(Z):
                      off.ctypes.data_as(ctypes.c_void_p), ctypes.byref(act), None)
     assert rc == 7
     assert L.zs_gemm_workspace_bytes(32, 28672, 4096) >= 32 * 28672 * 4
+
+
+def test_gemm_path_and_workspace_sizes(Z):
+    # include/zs.h: M <= ZS_GEMM_LARGE_M runs the fused kernel with the fp32 split-K
+    # workspace; larger M runs the decoupled path whose workspace holds the decoded W.
+    L = Z.lib()
+    hdr = open(os.path.join(ROOT, "include", "zs.h")).read()
+    large = int(re.search(r"#define ZS_GEMM_LARGE_M (\d+)", hdr).group(1))
+    N, K = 28672, 4096
+    for M in (1, 8, 32, large):
+        assert L.zs_gemm_is_decoupled(M) == 0
+        ws = L.zs_gemm_workspace_bytes(M, N, K)
+        assert ws >= 4 * min(M, 256) * N and ws % 256 == 0
+    for M in (large + 1, 1024, 8192):
+        assert L.zs_gemm_is_decoupled(M) == 1
+        assert L.zs_gemm_workspace_bytes(M, N, K) >= 2 * N * K
+    assert L.zs_gemm_workspace_bytes(0, N, K) == 0
+    # K is padded to a multiple of 8 elements (16-B rows of the decoded operand)
+    assert L.zs_gemm_workspace_bytes(large + 1, 100, 1001) >= 2 * 100 * 1008
