@@ -18,7 +18,7 @@ namespace {
 thread_local int g_last_launches = 0;
 unsigned long long* g_trace = nullptr;  // debug: set by zs_debug_set_trace
 uint32_t g_dbg = 0;                     // debug: experiment flags (zs_debug_set_flags)
-uint32_t g_max_cslots = 3;              // ring depth cap (tunable via zs_debug_set_ring)
+uint32_t g_max_cslots = 16;             // ring depth cap (tunable via zs_debug_set_ring)
 int64_t g_large_m = ZS_GEMM_LARGE_M;    // decoupled-path threshold (zs_debug_set_large_m)
 
 // cuBLAS handle of the decoupled prefill path: one per (host thread, device), created on
@@ -264,8 +264,8 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
     // smem split: compressed ring stages first (2..max, ~48 KB each at r = 0.98), X ring
     // gets the rest (up to 16 tiles, at least 2)
     const size_t base = zs::gemm_fixed_smem();
-    uint32_t nc = (uint32_t)std::min<size_t>(
-        zs::gemm_max_cslots(), (budget - base - (size_t)zs::gemm_units_per_stage() * p.aslot_bytes) / p.cslot_bytes);
+    const size_t xmin = (size_t)std::max(8, 2 * zs::gemm_units_per_stage()) * p.aslot_bytes;   // >= 8 X tiles
+    uint32_t nc = (uint32_t)std::min<size_t>(zs::gemm_max_cslots(), (budget - base - xmin) / p.cslot_bytes);
     nc = std::min<uint32_t>(nc, g_max_cslots);
     uint32_t nx = (uint32_t)std::min<size_t>(zs::gemm_max_xslots(), (budget - base - nc * (size_t)p.cslot_bytes) / p.aslot_bytes);
     nx -= nx % (uint32_t)zs::gemm_units_per_stage();
@@ -279,7 +279,7 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
     p.n_aslots = na - na % 4;
     auto magic = [](uint32_t d) { return d <= 1u ? 0u : (uint32_t)((1ull << 32) / d + 1ull); };
     p.cdiv_magic = magic(p.n_cslots);
-    p.adiv_magic = magic(p.n_aslots / 4);
+    p.adiv_magic = magic(p.n_aslots / (uint32_t)zs::gemm_units_per_stage());
     if (p.n_umma != cur_box) {
       cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
       cuuint64_t strides[1] = {(cuuint64_t)(ldx * 2)};

@@ -478,6 +478,48 @@ __device__ __forceinline__ uint4 decode_row_abs(uint32_t b1, uint32_t b2, uint32
   return make_uint4(out[0], out[1], out[2], out[3]);
 }
 
+// Same as decode_row_abs with the fallback-merge selectors read from the table (fsel word j =
+// the high half of ent word j, pre-shifted) instead of extracted per word: 3 issue slots
+// fewer per row for one more 16-B table load.
+__device__ __forceinline__ uint4 decode_row_abs2(uint32_t b1, uint32_t b2, uint32_t b3, uint32_t m, uint4 ent,
+                                                 uint4 fsel, const uint32_t* __restrict__ H32, uint32_t hsh8,
+                                                 const uint16_t* __restrict__ Lrow, uint32_t eb7x2) {
+  const uint32_t h0 = H32[0], h1 = H32[1], h2 = H32[2];
+  const uint32_t hlo = __funnelshift_r(h0, h1, hsh8);
+  const uint32_t hhi = __funnelshift_r(h1, h2, hsh8);
+  // first two fallback values (FMA pipe: the ALU pipe is the decoder's bottleneck)
+  const uint32_t lpair = mad_lo(Lrow[1], ZS_MUL(kM16, 1u << 16), Lrow[0]);
+  uint32_t l1, u1, l2, u2, l3, u3;
+  spread_plane<0>(b1, l1, u1);
+  spread_plane<1>(b2, l2, u2);
+  spread_plane<2>(b3, l3, u3);
+  const uint32_t WA = (l1 & 0x01010101u) | (l2 & 0x02020202u) | (l3 & 0x04040404u);
+  const uint32_t WB = (u1 & 0x10101010u) | (u2 & 0x20202020u) | (u3 & 0x40404040u);
+  const uint32_t E[4] = {mad_lo(WA, ZS_MUL(kM7, 128u), eb7x2), mad_hi(WA, ZS_MUL(kM31, 1u << 31), eb7x2),
+                         mad_lo(WB, ZS_MUL(kM3, 8u), eb7x2), mad_hi(WB, ZS_MUL(kM27, 1u << 27), eb7x2)};
+  const uint32_t sel[4] = {ent.x, ent.y, ent.z, ent.w};
+  const uint32_t fs[4] = {fsel.x, fsel.y, fsel.z, fsel.w};
+  uint32_t out[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t P = prmt(hlo, hhi, sel[j]);
+    const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);
+    out[j] = prmt(lpair, w, fs[j]);
+  }
+  if (ent.x & 0x80u) {  // rank >= 2 fallbacks: rare patch loop
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t rank = (uint32_t)i - __popc(m & ((1u << i) - 1u));
+      if (!((m >> i) & 1u) && rank >= 2) {
+        const uint32_t v = Lrow[rank];
+        const int j = i >> 1;
+        out[j] = (i & 1) ? ((out[j] & 0x0000FFFFu) | (v << 16)) : ((out[j] & 0xFFFF0000u) | v);
+      }
+    }
+  }
+  return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
 __device__ __forceinline__ uint4 decode_row_core(uint32_t b1, uint32_t b2, uint32_t b3, uint32_t m, uint4 ent,
                                                  const uint8_t* __restrict__ H, uint32_t hs,
                                                  const uint16_t* __restrict__ L, uint32_t ls, uint32_t eb7x2) {

@@ -141,8 +141,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Bars* bars = reinterpret_cast<Bars*>(smem);
   uint8_t* rptab = smem + 1024;                        // decoder row-prefix tables
-  uint4* slut = reinterpret_cast<uint4*>(smem + 1024 + kRpTabBytes);   // PRMT selector table
-  uint8_t* xslots = smem + 1024 + kRpTabBytes + 4096;
+  uint4* slut = reinterpret_cast<uint4*>(smem + 1024 + kRpTabBytes);   // PRMT selectors, 2 x 16 B per m
+  uint8_t* xslots = smem + 1024 + kRpTabBytes + 8192;
   uint8_t* cslots = xslots + (size_t)p.n_xslots * p.aslot_bytes;
 
   const int tid = threadIdx.x;
@@ -164,7 +164,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t band0 = u0 / nbc, kc0 = u0 % nbc;
 
   // ---- setup
-  if (tid < 256) slut[tid] = c_lut[tid];
+  if (tid < 256) {
+    const uint4 e = c_lut[tid];
+    slut[2 * tid] = e;
+    slut[2 * tid + 1] = make_uint4(e.x >> 16, e.y >> 16, e.z >> 16, e.w >> 16);
+  }
   if (tid < (int)p.n_cslots) reinterpret_cast<uint32_t*>(cslots + (size_t)tid * p.cslot_bytes)[24] = 0xFFFFFFFFu;
   if (tid == 32) {
     for (uint32_t i = 0; i < S_c; ++i) {
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // the quad of lanes of a stage computes the stage header with shuffles.
     const uint64_t pol = policy_evict_first();
     const ulonglong2* off2 = reinterpret_cast<const ulonglong2*>(p.offsets);
-    const int quad = lane >> 2, qi = lane & 3;
+    const int quad = lane / kUPS, qi = lane % kUPS;   // lane group of a stage / unit in it
     uint32_t slot = 0, eph = 1;   // ring slot / empty-barrier parity of the next stage
     for (int b0 = 0; b0 < nunits; b0 += 32) {
       const int it = b0 + lane;
@@ -221,7 +225,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t pha = h1a - h0a, phb = h1b - h0b, pla = l1a - l0a, plb = l1b - l0b;
       const uint32_t tot_self = pha + phb + pla + plb + (valid ? (has_b ? 3072u : 1536u) : 0u);
 #pragma unroll
-      for (int d = 1; d < 4; d <<= 1) {
+      for (int d = 1; d < kUPS; d <<= 1) {
         const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, pha, d), b = __shfl_up_sync(0xFFFFFFFFu, phb, d);
         const uint32_t c = __shfl_up_sync(0xFFFFFFFFu, pla, d), e = __shfl_up_sync(0xFFFFFFFFu, plb, d);
         if (qi >= d) { pha += a; phb += b; pla += c; plb += e; }
@@ -229,15 +233,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // pha.. are now inclusive; exclusive = inclusive - own size
       const uint32_t oha = pha - (h1a - h0a), ohb = phb - (h1b - h0b), ola = pla - (l1a - l0a), olb = plb - (l1b - l0b);
       uint32_t stage_bytes = tot_self;
-      stage_bytes += __shfl_xor_sync(0xFFFFFFFFu, stage_bytes, 1);
-      stage_bytes += __shfl_xor_sync(0xFFFFFFFFu, stage_bytes, 2);
+#pragma unroll
+      for (int d = 1; d < kUPS; d <<= 1) stage_bytes += __shfl_xor_sync(0xFFFFFFFFu, stage_bytes, d);
       // runs of same-band units inside the quad: a run starts at qi == 0 or on a band change
       const uint32_t band_prev = __shfl_up_sync(0xFFFFFFFFu, band, 1);
       const bool run_start = valid && (qi == 0 || band_prev != band);
       const uint32_t starts = __ballot_sync(0xFFFFFFFFu, run_start);
       const uint32_t validm = __ballot_sync(0xFFFFFFFFu, valid);
       // last lane of my run: next start in my quad minus one (or the quad's last valid lane)
-      const uint32_t quad_mask = 0xFu << (4 * quad);
+      const uint32_t quad_mask = ((1u << kUPS) - 1u) << (kUPS * quad);
       const uint32_t later = starts & quad_mask & ~((2u << lane) - 1u);
       const uint32_t qvalid = validm & quad_mask;
       const int qlast = qvalid ? 31 - __clz(qvalid) : lane;
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               const uint32_t b2 = pb[cf * 8u + kUPS * 512];
               const uint32_t b3 = pb[cf * 8u + 2 * kUPS * 512];
               const uint32_t m = b1 | b2 | b3;
-              v[qq] = decode_row_abs(b1, b2, b3, m, slut[m],
+              v[qq] = decode_row_abs2(b1, b2, b3, m, slut[2 * m], slut[2 * m + 1],
                                      reinterpret_cast<const uint32_t*>(smem + (hs_abs & ~3u)), hs_abs * 8u,
                                      reinterpret_cast<const uint16_t*>(smem + mad_lo(hs_abs, ZS_MUL(kMNeg2, 0xFFFFFFFEu), la0 + 128u * cf)),
                                      p.eb7x2);
@@ -652,7 +656,7 @@ cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, 
 }
 
 size_t gemm_smem_bytes(const GemmParams& p) {
-  return 1024 /*align slack*/ + 1024 + kRpTabBytes + 4096 + (size_t)p.n_xslots * p.aslot_bytes +
+  return 1024 /*align slack*/ + 1024 + kRpTabBytes + 8192 + (size_t)p.n_xslots * p.aslot_bytes +
          (size_t)p.n_cslots * p.cslot_bytes;
 }
 
@@ -663,6 +667,6 @@ int gemm_max_aslots() { return kMaxASlots; }
 uint32_t gemm_stage_fixed_bytes() { return kStageMeta + kStagePlanes; }
 int gemm_units_per_stage() { return kUPS; }
 int gemm_max_chunk() { return 128; }
-uint32_t gemm_fixed_smem() { return 1024 + 1024 + kRpTabBytes + 4096; }
+uint32_t gemm_fixed_smem() { return 1024 + 1024 + kRpTabBytes + 8192; }
 
 }  // namespace zs
