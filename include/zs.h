@@ -153,6 +153,25 @@ zs_status zs_gemm(const uint16_t *x, int64_t ldx, const zs_tensor *w, uint16_t *
                   int64_t M, int64_t N, int64_t K, void *workspace, size_t workspace_bytes,
                   void *stream);
 
+/* GPU-side encoder: the same bytes as zs_encode_measure / zs_encode (Alg. 1,
+ * P:306-333; canonical order S:277), computed on the device from a DEVICE matrix w (row-major,
+ * leading dimension ld >= cols, BF16 bit patterns).  Kernels: exponent histogram, per-BlockTile
+ * in-window counts, and one warp per BlockTile packing the bit-planes and the H / L segments;
+ * the window choice and the offsets prefix run on the host over the copied-back counts.
+ * Both calls are SYNCHRONOUS on `stream` (they return host-side sizes).  All output pointers
+ * of zs_encode_device are device buffers with the capacities of `cap` (zs_encode_bound or the
+ * exact sizes from zs_encode_measure_device); offsets receives n_blocktiles + 1 pairs.
+ * ws: device scratch of zs_encode_device_workspace_bytes(rows, cols) bytes.
+ * Errors: as zs_encode, plus ZS_ERR_CAPACITY (workspace), ZS_ERR_UNSUPPORTED, ZS_ERR_CUDA. */
+size_t zs_encode_device_workspace_bytes(int64_t rows, int64_t cols);
+zs_status zs_encode_measure_device(const uint16_t *w, int64_t rows, int64_t cols, int64_t ld, void *ws,
+                                   size_t ws_bytes, void *stream, int32_t *base_exp, int64_t *covered,
+                                   zs_sizes *exact);
+zs_status zs_encode_device(const uint16_t *w, int64_t rows, int64_t cols, int64_t ld, int32_t base_exp,
+                           const zs_sizes *cap, uint64_t *b1, uint64_t *b2, uint64_t *b3, uint8_t *h,
+                           uint16_t *l, uint64_t *offsets, zs_sizes *actual, uint16_t *pad_word, void *ws,
+                           size_t ws_bytes, void *stream);
+
 /* Number of kernel launches the most recent successful zs_gemm / zs_decompress call on
  * this thread issued (for the bench's gpu_launches count). */
 int zs_last_launch_count(void);

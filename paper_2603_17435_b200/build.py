@@ -14,9 +14,9 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libzs.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CU_SOURCES = ["zs_api.cu", "zs_decompress.cu", "zs_gemm.cu"]
+CU_SOURCES = ["zs_api.cu", "zs_decompress.cu", "zs_gemm.cu", "zs_encode_gpu.cu"]
 CPP_SOURCES = ["zs_encode.cpp"]
-HEADERS = ["zs_device.cuh", "zs_kernels.h"]
+HEADERS = ["zs_device.cuh", "zs_kernels.h", "zs_host.h", "zs_lut.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]

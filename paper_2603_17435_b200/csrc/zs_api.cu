@@ -11,7 +11,10 @@
 #include <mutex>
 
 #include "../../include/zs.h"
+#include "zs_host.h"
 #include "zs_kernels.h"
+
+#include <vector>
 
 namespace {
 
@@ -297,5 +300,88 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
     ++launches;
   }
   g_last_launches = launches;
+  return ZS_OK;
+}
+
+// ------------------------------------------------------------------ GPU encoder (f3)
+extern "C" size_t zs_encode_device_workspace_bytes(int64_t rows, int64_t cols) {
+  if (rows < 1 || cols < 1) return 0;
+  const int64_t nbt = (up(rows, 64) / 64) * (up(cols, 64) / 64);
+  return (size_t)(256 * 8 + up(nbt * 4, 256));
+}
+
+namespace {
+zs_status encode_counts(const uint16_t* w, int64_t rows, int64_t cols, int64_t ld, int lo, int hi, void* ws,
+                        cudaStream_t s, std::vector<uint32_t>& hcnt) {
+  const int64_t nbc = up(cols, 64) / 64, nbt = (up(rows, 64) / 64) * nbc;
+  uint32_t* dcnt = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(ws) + 256 * 8);
+  if (zs::launch_encode_count(w, rows, cols, ld, nbc, nbt, lo, hi, dcnt, s) != cudaSuccess) return ZS_ERR_CUDA;
+  hcnt.resize(nbt);
+  if (cudaMemcpyAsync(hcnt.data(), dcnt, nbt * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ZS_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return ZS_ERR_CUDA;
+  return ZS_OK;
+}
+}  // namespace
+
+extern "C" zs_status zs_encode_measure_device(const uint16_t* w, int64_t rows, int64_t cols, int64_t ld, void* ws,
+                                              size_t ws_bytes, void* stream, int32_t* base_exp, int64_t* covered,
+                                              zs_sizes* exact) {
+  g_last_launches = 0;
+  if (!w || rows < 1 || cols < 1 || ld < cols || !base_exp || !exact || !ws) return ZS_ERR_INVALID_ARG;
+  if (ws_bytes < zs_encode_device_workspace_bytes(rows, cols)) return ZS_ERR_CAPACITY;
+  int sms = 0;
+  zs_status st = device_check(&sms);
+  if (st != ZS_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* dh = reinterpret_cast<unsigned long long*>(ws);
+  if (cudaMemsetAsync(dh, 0, 256 * 8, s) != cudaSuccess) return ZS_ERR_CUDA;
+  if (zs::launch_encode_hist(w, rows, cols, ld, dh, sms, s) != cudaSuccess) return ZS_ERR_CUDA;
+  unsigned long long hh[256];
+  if (cudaMemcpyAsync(hh, dh, sizeof(hh), cudaMemcpyDeviceToHost, s) != cudaSuccess) return ZS_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return ZS_ERR_CUDA;
+  int64_t hist[256];
+  for (int i = 0; i < 256; ++i) hist[i] = (int64_t)hh[i];
+  int64_t best = 0;
+  const int s0 = zs::window_start(hist, &best);
+  *base_exp = s0 - 1;
+  if (covered) *covered = best;
+  std::vector<uint32_t> hcnt;
+  if ((st = encode_counts(w, rows, cols, ld, s0, s0 + 6, ws, s, hcnt)) != ZS_OK) return st;
+  zs::sizes_and_offsets(rows, cols, hcnt.data(), exact, nullptr);
+  g_last_launches = 2;
+  return ZS_OK;
+}
+
+extern "C" zs_status zs_encode_device(const uint16_t* w, int64_t rows, int64_t cols, int64_t ld, int32_t base_exp,
+                                      const zs_sizes* cap, uint64_t* b1, uint64_t* b2, uint64_t* b3, uint8_t* h,
+                                      uint16_t* l, uint64_t* offsets, zs_sizes* actual, uint16_t* pad_word, void* ws,
+                                      size_t ws_bytes, void* stream) {
+  g_last_launches = 0;
+  if (!w || rows < 1 || cols < 1 || ld < cols || !cap || !b1 || !b2 || !b3 || !offsets || !actual || !ws)
+    return ZS_ERR_INVALID_ARG;
+  if (base_exp < -1 || base_exp > 248) return ZS_ERR_INVALID_ARG;
+  if (ws_bytes < zs_encode_device_workspace_bytes(rows, cols)) return ZS_ERR_CAPACITY;
+  int sms = 0;
+  zs_status st = device_check(&sms);
+  if (st != ZS_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<uint32_t> hcnt;
+  if ((st = encode_counts(w, rows, cols, ld, base_exp + 1, base_exp + 7, ws, s, hcnt)) != ZS_OK) return st;
+  const int64_t nbc = up(cols, 64) / 64, nbt = (up(rows, 64) / 64) * nbc;
+  zs_sizes sz;
+  std::vector<uint64_t> off(2 * (nbt + 1));
+  zs::sizes_and_offsets(rows, cols, hcnt.data(), &sz, off.data());
+  if (cap->n_fragtiles < sz.n_fragtiles || cap->n_blocktiles < sz.n_blocktiles || cap->h_bytes < sz.h_bytes ||
+      cap->l_words < sz.l_words)
+    return ZS_ERR_CAPACITY;
+  if ((sz.h_bytes && !h) || (sz.l_words && !l)) return ZS_ERR_INVALID_ARG;
+  if (cudaMemcpyAsync(offsets, off.data(), off.size() * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return ZS_ERR_CUDA;
+  if (zs::launch_encode_pack(w, rows, cols, ld, nbc, nbt, base_exp, offsets, b1, b2, b3, h, l, s) != cudaSuccess)
+    return ZS_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return ZS_ERR_CUDA;   // `off` must outlive the copy
+  *actual = sz;
+  if (pad_word) *pad_word = (uint16_t)((base_exp + 1) << 7);
+  g_last_launches = 2;
   return ZS_OK;
 }

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../../include/zs.h"
+#include "zs_host.h"
 
 namespace {
 
@@ -87,6 +88,44 @@ void sizes_from_counts(const Geo& g, const std::vector<int64_t>& hcnt, zs_sizes*
 
 }  // namespace
 
+namespace zs {
+
+// 7 consecutive exponents with maximum coverage, first start wins ties (Alg. 1 line 3)
+int window_start(const int64_t hist[256], int64_t* covered) {
+  int64_t run = 0;
+  for (int e = 0; e < 7; ++e) run += hist[e];
+  int64_t best = run;
+  int best_s = 0;
+  for (int s = 1; s <= 249; ++s) {
+    run += hist[s + 6] - hist[s - 1];
+    if (run > best) {
+      best = run;
+      best_s = s;
+    }
+  }
+  if (covered) *covered = best;
+  return best_s;
+}
+
+void sizes_and_offsets(int64_t rows, int64_t cols, const uint32_t* hcnt, zs_sizes* s, uint64_t* offsets) {
+  const Geo g = make_geo(rows, cols, cols);
+  std::vector<int64_t> h(hcnt, hcnt + g.nbt);
+  sizes_from_counts(g, h, s);
+  if (offsets) {
+    uint64_t ho = 0, lo = 0;
+    for (int64_t b = 0; b < g.nbt; ++b) {
+      offsets[2 * b] = ho;
+      offsets[2 * b + 1] = lo;
+      ho += (uint64_t)up(hcnt[b], 16);
+      lo += (uint64_t)up(2 * (4096 - (int64_t)hcnt[b]), 16);
+    }
+    offsets[2 * g.nbt] = ho;
+    offsets[2 * g.nbt + 1] = lo;
+  }
+}
+
+}  // namespace zs
+
 extern "C" zs_status zs_encode_bound(int64_t rows, int64_t cols, zs_sizes* s) {
   if (rows < 1 || cols < 1 || !s) return ZS_ERR_INVALID_ARG;
   const Geo g = make_geo(rows, cols, cols);
@@ -125,18 +164,8 @@ extern "C" zs_status zs_encode_measure(const uint16_t* w, int64_t rows, int64_t 
   int64_t hist[256] = {0};
   for (auto& h : part)
     for (int e = 0; e < 256; ++e) hist[e] += h[e];
-  // 7 consecutive exponents with maximum coverage, first start wins ties (line 3)
-  int64_t run = 0;
-  for (int e = 0; e < 7; ++e) run += hist[e];
-  int64_t best = run;
-  int best_s = 0;
-  for (int s = 1; s <= 249; ++s) {
-    run += hist[s + 6] - hist[s - 1];
-    if (run > best) {
-      best = run;
-      best_s = s;
-    }
-  }
+  int64_t best = 0;
+  const int best_s = zs::window_start(hist, &best);
   *base_exp = best_s - 1;  // line 4
   if (covered) *covered = best;
   std::vector<int64_t> hcnt(g.nbt);

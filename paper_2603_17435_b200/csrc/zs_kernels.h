@@ -71,4 +71,13 @@ int gemm_units_per_stage();
 int gemm_max_chunk();
 uint32_t gemm_fixed_smem();
 
+// GPU encoder (zs_encode_gpu.cu)
+cudaError_t launch_encode_hist(const uint16_t* w, int64_t rows, int64_t cols, int64_t ld, unsigned long long* hist,
+                               int sms, cudaStream_t s);
+cudaError_t launch_encode_count(const uint16_t* w, int64_t rows, int64_t cols, int64_t ld, int64_t nbc, int64_t nbt,
+                                int lo, int hi, uint32_t* hcnt, cudaStream_t s);
+cudaError_t launch_encode_pack(const uint16_t* w, int64_t rows, int64_t cols, int64_t ld, int64_t nbc, int64_t nbt,
+                               int32_t base_exp, const uint64_t* offsets, uint64_t* b1, uint64_t* b2, uint64_t* b3,
+                               uint8_t* h, uint16_t* l, cudaStream_t s);
+
 }  // namespace zs

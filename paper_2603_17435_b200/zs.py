@@ -20,7 +20,8 @@ ZS_STATUS = {0: "ZS_OK", 1: "ZS_ERR_INVALID_ARG", 2: "ZS_ERR_SHAPE", 3: "ZS_ERR_
 
 # every symbol include/zs.h declares (checked by tests/test_abi.py)
 EXPORTS = ["zs_encode_bound", "zs_encode_measure", "zs_encode", "zs_decompress", "zs_gemm_workspace_bytes",
-           "zs_gemm_is_decoupled", "zs_gemm", "zs_last_launch_count", "zs_status_string"]
+           "zs_gemm_is_decoupled", "zs_gemm", "zs_last_launch_count", "zs_status_string",
+           "zs_encode_device_workspace_bytes", "zs_encode_measure_device", "zs_encode_device"]
 
 
 class ZsError(RuntimeError):
@@ -66,7 +67,15 @@ def lib():
         L.zs_gemm.argtypes = [vp, i64, ctypes.POINTER(zs_tensor), vp, i64, i64, i64, i64, vp, ctypes.c_size_t, vp]
         L.zs_status_string.argtypes = [ctypes.c_int]
         L.zs_status_string.restype = ctypes.c_char_p
-        for f in ("zs_encode_bound", "zs_encode_measure", "zs_encode", "zs_decompress", "zs_gemm"):
+        L.zs_encode_device_workspace_bytes.argtypes = [i64, i64]
+        L.zs_encode_device_workspace_bytes.restype = ctypes.c_size_t
+        L.zs_encode_measure_device.argtypes = [vp, i64, i64, i64, vp, ctypes.c_size_t, vp, ctypes.POINTER(i32),
+                                               ctypes.POINTER(i64), ctypes.POINTER(zs_sizes)]
+        L.zs_encode_device.argtypes = [vp, i64, i64, i64, i32, ctypes.POINTER(zs_sizes), vp, vp, vp, vp, vp, vp,
+                                       ctypes.POINTER(zs_sizes), ctypes.POINTER(ctypes.c_uint16), vp, ctypes.c_size_t,
+                                       vp]
+        for f in ("zs_encode_bound", "zs_encode_measure", "zs_encode", "zs_decompress", "zs_gemm",
+                  "zs_encode_measure_device", "zs_encode_device"):
             getattr(L, f).restype = ctypes.c_int
         L.zs_last_launch_count.restype = ctypes.c_int
         _lib = L
@@ -200,6 +209,43 @@ class ZsDevice:
         t.b1, t.b2, t.b3 = self.b1.data_ptr(), self.b2.data_ptr(), self.b3.data_ptr()
         t.h, t.l, t.offsets = self.h.data_ptr(), self.l.data_ptr(), self.offsets.data_ptr()
         return t
+
+
+def encode_device(w, base_exp: int | None = None, stream=None) -> "ZsDevice":
+    """GPU-side encoder: a device torch.bfloat16 [rows][cols] matrix -> ZsDevice on the same
+    device, byte-identical to encode(w.cpu()).to(device)."""
+    import torch
+    assert w.dtype == torch.bfloat16 and w.dim() == 2 and w.stride(1) == 1 and w.is_cuda
+    L = lib()
+    rows, cols = w.shape
+    dev = w.device
+    sp = _stream_ptr(stream, dev)
+    wsb = int(L.zs_encode_device_workspace_bytes(rows, cols))
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)
+    wp = ctypes.c_void_p(w.data_ptr())
+    sz = zs_sizes()
+    be = ctypes.c_int32()
+    cov = ctypes.c_int64()
+    _check("zs_encode_measure_device", L.zs_encode_measure_device(wp, rows, cols, w.stride(0), ctypes.c_void_p(ws.data_ptr()),
+                                                                  ws.numel(), sp, ctypes.byref(be), ctypes.byref(cov),
+                                                                  ctypes.byref(sz)))
+    if base_exp is not None and base_exp != be.value:
+        be = ctypes.c_int32(base_exp)
+        _check("zs_encode_bound", L.zs_encode_bound(rows, cols, ctypes.byref(sz)))
+    nft, nbt = sz.n_fragtiles, sz.n_blocktiles
+    planes = [torch.empty(nft, dtype=torch.int64, device=dev) for _ in range(3)]
+    h = torch.empty(max(sz.h_bytes, 16), dtype=torch.uint8, device=dev)
+    l = torch.empty(max(sz.l_words, 8), dtype=torch.int16, device=dev)
+    off = torch.empty(2 * (nbt + 1), dtype=torch.int64, device=dev)
+    act = zs_sizes()
+    pad = ctypes.c_uint16()
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr())
+    _check("zs_encode_device", L.zs_encode_device(wp, rows, cols, w.stride(0), be.value, ctypes.byref(sz),
+                                                  ptr(planes[0]), ptr(planes[1]), ptr(planes[2]), ptr(h), ptr(l),
+                                                  ptr(off), ctypes.byref(act), ctypes.byref(pad),
+                                                  ctypes.c_void_p(ws.data_ptr()), ws.numel(), sp))
+    sizes = {f: getattr(act, f) for f, _ in zs_sizes._fields_}
+    return ZsDevice(sizes, be.value, pad.value, planes[0], planes[1], planes[2], h, l, off)
 
 
 def _stream_ptr(stream, device):
