@@ -120,31 +120,34 @@ zs_status zs_decompress(const zs_tensor *w, uint16_t *out, int64_t ld_out, void 
 /* Token count above which zs_gemm takes the decoupled prefill path ("decoupled
  * decompression + dense GEMM for the compute-bound prefill stage"): zs_decompress of W
  * into the workspace, then one dense BF16 tensor-core GEMM (cuBLAS, fp32 accumulate).
- * At or below it the fused ZipGEMM kernel runs (decode stage).  Value measured on B200,
- * see DESIGN.md (crossover of the two paths over LLaMA-3.1-8B layer shapes). */
+ * At or below it the fused ZipGEMM kernel runs (decode stage).  Values measured on B200,
+ * see DESIGN.md 7.3 (crossover of the two paths over LLaMA-3.1-8B layer shapes): matrices
+ * of at most ZS_GEMM_SMALL_NK elements switch at ZS_GEMM_LARGE_M_SMALL_NK tokens. */
 #define ZS_GEMM_LARGE_M 128
+#define ZS_GEMM_SMALL_NK (32ll * 1024 * 1024)
+#define ZS_GEMM_LARGE_M_SMALL_NK 32
 
 /* Workspace (device bytes) zs_gemm needs for an M x N x K problem.
- *   M <= ZS_GEMM_LARGE_M: fp32 split-K partial sums [M][N] plus per-band arrival
+ *   fused path (zs_gemm_is_decoupled == 0): fp32 split-K partial sums [M][N] plus per-band arrival
  *     counters.  It must be zero-filled once before its first use; zs_gemm leaves it
  *     zero-filled again when it completes, so one workspace can be reused by every later
  *     call on the same stream.
- *   M >  ZS_GEMM_LARGE_M: scratch for the decoded weight, N x roundup(K, 8) BF16.  Any
+ *   decoupled path: scratch for the decoded weight, N x roundup(K, 8) BF16.  Any
  *     contents on entry; NOT zero on exit, so do not hand the same buffer to a fused
  *     call afterwards without zero-filling it (zs_gemm_is_decoupled tells the paths apart).
  * Returns 0 for non-positive sizes. */
 size_t zs_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 
-/* 1 if zs_gemm takes the decoupled path for this token count (M > ZS_GEMM_LARGE_M), else
- * 0.  Host, O(1), no errors. */
-int zs_gemm_is_decoupled(int64_t M);
+/* 1 if zs_gemm takes the decoupled path for this problem (M above the shape's threshold, see
+ * ZS_GEMM_LARGE_M), else 0.  Host, O(1), no errors. */
+int zs_gemm_is_decoupled(int64_t M, int64_t N, int64_t K);
 
 /* ZipGEMM: Y[M][N] = X[M][K] * W[N][K]^T with fp32 accumulation in tensor
  * memory and BF16 output (RNE).  x: device BF16, row-major, leading dimension ldx
  * (elements), base 16-byte aligned and ldx*2 % 16 == 0 (TMA rule).  w: DEVICE tensor with
  * w->sz.rows == N, w->sz.cols == K.  y: device BF16 [M][ldy], ldy >= N.  Outputs of
- * padded rows are not written.  M >= 1: M <= ZS_GEMM_LARGE_M runs the fused kernel (one
- * launch); larger M runs zs_decompress + a cuBLAS BF16 GEMM on the same stream (the
+ * padded rows are not written.  M >= 1: small M runs the fused kernel (one launch); M above
+ * the shape's threshold (ZS_GEMM_LARGE_M) runs zs_decompress + a cuBLAS BF16 GEMM on the same stream (the
  * library keeps one cuBLAS handle per host thread and device, created on first use).
  * workspace: see zs_gemm_workspace_bytes.
  * Errors: ZS_ERR_INVALID_ARG, ZS_ERR_SHAPE, ZS_ERR_ALIGNMENT, ZS_ERR_CAPACITY

@@ -22,7 +22,7 @@ thread_local int g_last_launches = 0;
 unsigned long long* g_trace = nullptr;  // debug: set by zs_debug_set_trace
 uint32_t g_dbg = 0;                     // debug: experiment flags (zs_debug_set_flags)
 uint32_t g_max_cslots = 16;             // ring depth cap (tunable via zs_debug_set_ring)
-int64_t g_large_m = ZS_GEMM_LARGE_M;    // decoupled-path threshold (zs_debug_set_large_m)
+int64_t g_large_m = -1;                 // forced decoupled-path threshold (zs_debug_set_large_m), -1 = per shape
 
 // cuBLAS handle of the decoupled prefill path: one per (host thread, device), created on
 // first use.  cuBLAS only runs the plain dense GEMM on the already-decoded weights.
@@ -33,7 +33,15 @@ cublasHandle_t blas_handle(int dev) {
   return h[dev];
 }
 
-bool use_decoupled(int64_t M) { return M > g_large_m; }
+// Fused for small M, decoupled above a per-shape threshold (measured on the 8B layers,
+// DESIGN.md 7.3): ZS_GEMM_LARGE_M for large matrices; for matrices of at most
+// ZS_GEMM_SMALL_NK elements the decompression is cheap and the fused kernel's fixed cost
+// dominates, so the crossover is ZS_GEMM_LARGE_M_SMALL_NK.
+bool use_decoupled(int64_t M, int64_t N, int64_t K) {
+  if (g_large_m >= 0) return M > g_large_m;
+  const int64_t thr = (N * K <= ZS_GEMM_SMALL_NK) ? ZS_GEMM_LARGE_M_SMALL_NK : ZS_GEMM_LARGE_M;
+  return M > thr;
+}
 
 inline int64_t up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -118,7 +126,7 @@ extern "C" void zs_debug_set_trace(unsigned long long* dev_buf) { g_trace = dev_
 extern "C" void zs_debug_set_flags(int flags) { g_dbg = (uint32_t)flags; }
 extern "C" void zs_debug_set_ring(int max_cslots) { g_max_cslots = (uint32_t)std::max(1, max_cslots); }
 // Debug hook: move the fused / decoupled threshold (crossover measurement); < 0 restores it.
-extern "C" void zs_debug_set_large_m(long long m) { g_large_m = m < 0 ? ZS_GEMM_LARGE_M : (int64_t)m; }
+extern "C" void zs_debug_set_large_m(long long m) { g_large_m = m < 0 ? -1 : (int64_t)m; }
 
 extern "C" zs_status zs_decompress(const zs_tensor* w, uint16_t* out, int64_t ld_out, void* stream) {
   g_last_launches = 0;
@@ -168,11 +176,11 @@ static size_t splitk_bytes(int64_t M, int64_t N) {
 extern "C" size_t zs_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   if (M < 1 || N < 1 || K < 1) return 0;
   // decoupled path: scratch for the decoded W [N][roundup(K,8)] bf16
-  if (use_decoupled(M)) return (size_t)up(N * up(K, 8) * 2, 256);
+  if (use_decoupled(M, N, K)) return (size_t)up(N * up(K, 8) * 2, 256);
   return splitk_bytes(M, N);
 }
 
-extern "C" int zs_gemm_is_decoupled(int64_t M) { return use_decoupled(M) ? 1 : 0; }
+extern "C" int zs_gemm_is_decoupled(int64_t M, int64_t N, int64_t K) { return use_decoupled(M, N, K) ? 1 : 0; }
 
 extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w, uint16_t* y, int64_t ldy, int64_t M,
                              int64_t N, int64_t K, void* workspace, size_t workspace_bytes, void* stream) {
@@ -188,7 +196,7 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
   int sms = 0;
   if ((st = device_check(&sms)) != ZS_OK) return st;
 
-  if (use_decoupled(M)) {
+  if (use_decoupled(M, N, K)) {
     // Large M (prefill): ZipServ-Decomp into the workspace, then a dense BF16 GEMM
     // on the tensor cores (cuBLAS).  The decode runs once per call instead of once per
     // 128-token chunk.

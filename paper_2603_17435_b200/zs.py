@@ -62,7 +62,7 @@ def lib():
         L.zs_decompress.argtypes = [ctypes.POINTER(zs_tensor), vp, i64, vp]
         L.zs_gemm_workspace_bytes.argtypes = [i64, i64, i64]
         L.zs_gemm_workspace_bytes.restype = ctypes.c_size_t
-        L.zs_gemm_is_decoupled.argtypes = [i64]
+        L.zs_gemm_is_decoupled.argtypes = [i64, i64, i64]
         L.zs_gemm_is_decoupled.restype = ctypes.c_int
         L.zs_gemm.argtypes = [vp, i64, ctypes.POINTER(zs_tensor), vp, i64, i64, i64, i64, vp, ctypes.c_size_t, vp]
         L.zs_status_string.argtypes = [ctypes.c_int]
@@ -276,7 +276,7 @@ def workspace(M: int, N: int, K: int, device):
     decoupled (large-M) path -- two separate buffers, since the latter is left dirty."""
     import torch
     need = int(lib().zs_gemm_workspace_bytes(M, N, K))
-    key = (str(device), int(lib().zs_gemm_is_decoupled(M)))
+    key = (str(device), int(lib().zs_gemm_is_decoupled(M, N, K)))
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
         ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)

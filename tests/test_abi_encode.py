@@ -132,14 +132,21 @@ def test_gemm_path_and_workspace_sizes(Z):
     L = Z.lib()
     hdr = open(os.path.join(ROOT, "include", "zs.h")).read()
     large = int(re.search(r"#define ZS_GEMM_LARGE_M (\d+)", hdr).group(1))
+    small_nk = eval(re.search(r"#define ZS_GEMM_SMALL_NK \((.*)\)", hdr).group(1).replace("ll", ""))
+    small_m = int(re.search(r"#define ZS_GEMM_LARGE_M_SMALL_NK (\d+)", hdr).group(1))
     N, K = 28672, 4096
+    assert N * K > small_nk
     for M in (1, 8, 32, large):
-        assert L.zs_gemm_is_decoupled(M) == 0
+        assert L.zs_gemm_is_decoupled(M, N, K) == 0
         ws = L.zs_gemm_workspace_bytes(M, N, K)
         assert ws >= 4 * min(M, 256) * N and ws % 256 == 0
     for M in (large + 1, 1024, 8192):
-        assert L.zs_gemm_is_decoupled(M) == 1
+        assert L.zs_gemm_is_decoupled(M, N, K) == 1
         assert L.zs_gemm_workspace_bytes(M, N, K) >= 2 * N * K
+    # small matrices (8B QKV: 6144 x 4096) switch earlier
+    assert 6144 * 4096 <= small_nk
+    assert L.zs_gemm_is_decoupled(small_m, 6144, 4096) == 0
+    assert L.zs_gemm_is_decoupled(small_m + 1, 6144, 4096) == 1
     assert L.zs_gemm_workspace_bytes(0, N, K) == 0
     # K is padded to a multiple of 8 elements (16-B rows of the decoded operand)
     assert L.zs_gemm_workspace_bytes(large + 1, 100, 1001) >= 2 * 100 * 1008
