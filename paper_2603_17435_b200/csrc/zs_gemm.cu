@@ -82,6 +82,9 @@ struct __align__(8) Bars {
 
 // debug trace: trace[(cta * kTraceUnits + unit) * 16 + event] = clock64, first kTraceCtas CTAs
 constexpr int kTraceCtas = 4, kTraceUnits = 128;
+#ifndef ZS_REGSPLIT
+#define ZS_REGSPLIT 0   // setmaxnreg 72/40 split: measured 2x slower (spills in the 40-register roles)
+#endif
 #ifndef ZS_TRACE
 #define ZS_TRACE 0   // build with -DZS_TRACE=1 for scripts/trace_gemm.py (costs issue slots)
 #endif
@@ -194,6 +197,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = bars->tmem_base;
+  // register budget: 24 decoder warps x 72 + 8 control / epilogue warps x 40 = the 64 K
+  // register file (the decoders rematerialise addresses at the 64-register default)
+#if ZS_REGSPLIT
+  if (warp < kWarpEpi0) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 72;");
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+  }
+#endif
   const uint32_t dcols = p.acc_cols;                   // accumulator buffer stride (columns)
   const uint32_t tmem_a = tmem_base + 2u * dcols;      // first A slot column
 

@@ -20,12 +20,14 @@ ap.add_argument("--rings", default="")
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--cublas", action="store_true")
 ap.add_argument("--modes", default="auto", help="comma list of auto,fused,decoupled (forces the zs_gemm path)")
+ap.add_argument("--flags", default="0", help="comma list of zs_debug_set_flags values (timing experiments)")
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 l2 = torch.cuda.get_device_properties(dev).L2_cache_size
 L = Z.lib()
 L.zs_debug_set_ring.argtypes = [ctypes.c_int]
 L.zs_debug_set_large_m.argtypes = [ctypes.c_longlong]
+L.zs_debug_set_flags.argtypes = [ctypes.c_int]
 MODE_THR = {"auto": -1, "fused": 1 << 40, "decoupled": 0}
 
 
@@ -69,14 +71,17 @@ for layer in a.layers.split(","):
     for M in [int(m) for m in a.ms.split(",")]:
         x = torch.randn((M, K), device=dev).to(torch.bfloat16)
         y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
-        for mode, ring in [(md, r) for md in a.modes.split(",")
-                           for r in ([int(r) for r in a.rings.split(",")] if a.rings else [0])]:
+        for mode, ring, fl in [(md, r, f) for md in a.modes.split(",")
+                               for r in ([int(r) for r in a.rings.split(",")] if a.rings else [0])
+                               for f in [int(f) for f in a.flags.split(",")]]:
             L.zs_debug_set_large_m(MODE_THR[mode])
+            L.zs_debug_set_flags(fl)
             ws = Z.workspace(M, N, K, dev)
             if ring:
                 L.zs_debug_set_ring(ring)
             us = timeit(lambda i: Z.gemm(x, comp[i % R], out=y, ws=ws), R)
-            rec = {"layer": layer, "M": M, "mode": mode, "ring": ring, "us": round(us, 2),
+            rec = {"layer": layer, "M": M, "mode": mode, "ring": ring, "flags": fl, "us": round(us, 2),
+                   "bits_per_el": round(zh.bits_per_element(), 3), "coverage": round(zh.covered / w.size, 4),
                    "tflops": round(2 * M * N * K / us / 1e6, 1),
                    "gbs": round((zh.nbytes() + 2 * M * K + 2 * M * N) / us / 1e3, 1)}
             if dense is not None:
@@ -85,3 +90,4 @@ for layer in a.layers.split(","):
                 rec["speedup"] = round(cu / us, 3)
             print(json.dumps(rec), flush=True)
             L.zs_debug_set_large_m(-1)
+            L.zs_debug_set_flags(0)

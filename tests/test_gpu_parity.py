@@ -210,3 +210,21 @@ def test_gemm_paths_forced(zs, mode, N, K, M):
     finally:
         L.zs_debug_set_large_m(-1)
     np.testing.assert_array_equal(y, O.round_bf16_array(O.gemm_f64(x, w)))
+
+
+# ----------------------------------------------------------------- column shards (8(e)) on one GPU
+@pytest.mark.parametrize("world", [2, 8])
+def test_column_shards_concat_exact(zs, world):
+    # every rank's shard (a byte range of the full encoding with rebased offsets, same e_base)
+    # through zs_gemm; concatenating the Y slices must equal the unsharded product exactly
+    from paper_2603_17435_b200 import dist as D
+    N, K, M = 2048, 1024, 32
+    w = G.integer_weights(N, K, seed=77)
+    x = G.integer_activations(M, K, seed=78)
+    full = zs.encode(w)
+    xs = to_dev(x)
+    parts = []
+    for r in range(world):
+        r0, r1 = D.shard_bounds(N, world, r)
+        parts.append(to_np(zs.gemm(xs, D.shard_rows(full, r0, r1).to(DEV))))
+    np.testing.assert_array_equal(np.concatenate(parts, axis=1), O.round_bf16_array(O.gemm_f64(x, w)))

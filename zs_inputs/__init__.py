@@ -33,6 +33,16 @@ LAYERS = {
     "Q32B.O": (8192, 5120),
     "Q32B.GateUp": (5120, 51200),
     "Q32B.Down": (25600, 5120),
+    # per-rank column shards of the 70B layers at 8 GPUs (N / 8 output features each, 8(e))
+    "L70B.QKV.w8": (8192, 1280),
+    "L70B.O.w8": (8192, 1024),
+    "L70B.GateUp.w8": (8192, 7168),
+    "L70B.Down.w8": (28672, 1024),
+    # LM head of LLaMA-3.1-8B (vocabulary 128256, P:493 lists the LM head among the layers)
+    "L8B.LMHead": (4096, 128256),
+    # fixed-cost probes: one unit (128 x 64) and one 128-row band of K = 4096
+    "T.1unit": (64, 128),
+    "T.1band": (4096, 128),
 }
 
 
