@@ -125,6 +125,8 @@ extern "C" void zs_debug_set_trace(unsigned long long* dev_buf) { g_trace = dev_
 // (timing experiments only: results are wrong with any flag set).
 extern "C" void zs_debug_set_flags(int flags) { g_dbg = (uint32_t)flags; }
 extern "C" void zs_debug_set_ring(int max_cslots) { g_max_cslots = (uint32_t)std::max(1, max_cslots); }
+// Debug hook: programmatic dependent launch of the fused kernel on (1, default) / off (0).
+extern "C" void zs_debug_set_pdl(int on) { zs::g_pdl = on ? 1 : 0; }
 // Debug hook: move the fused / decoupled threshold (crossover measurement); < 0 restores it.
 extern "C" void zs_debug_set_large_m(long long m) { g_large_m = m < 0 ? -1 : (int64_t)m; }
 

@@ -98,6 +98,11 @@ __device__ __forceinline__ void trace_ev(unsigned long long* tr, int unit, int e
 #endif
 }
 
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -196,6 +201,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // Programmatic dependent launch: the next kernel on the stream may be scheduled now; its
+  // CTAs become resident as ours exit, and it reads nothing of ours before its own
+  // griddepcontrol.wait.  Weights and offsets are immutable, so the prologue and the
+  // compressed stream of this kernel start before the previous kernel has finished.
+  grid_launch_dependents();
   const uint32_t tmem_base = bars->tmem_base;
   // register budget: 24 decoder warps x 72 + 8 control / epilogue warps x 40 = the 64 K
   // register file (the decoders rematerialise addresses at the 64-register default)
@@ -312,6 +322,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t xbytes = p.n_umma * 128u;
     uint32_t kc = kc0;
     uint32_t xr = 0, xuse = 0;   // X ring stage of st / how often the ring has wrapped
+    grid_dependency_wait();      // X may be the previous kernel's output (PDL)
     for (int st = 0; st < nstages; ++st) {
       if (xuse > 0) mbar_wait(&bars->xempty[xr], (xuse - 1u) & 1u);
       const int nu = min(kUPS, nunits - st * kUPS);
@@ -589,6 +600,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // sleep on the named barrier the MMA warp arrives at once the segment's MMAs are
       // complete; the mbarrier wait after it then passes at once (and orders the TMEM reads)
       named_bar_sync(2 + (seg & 1), 160);
+      if (seg == 0) grid_dependency_wait();   // Y / workspace / counters: previous kernel done (PDL)
       mbar_wait(&bars->accfull[seg & 1], ((uint32_t)seg >> 1) & 1u);
       tc_fence_after();
       const int64_t n = (int64_t)band * 128 + et;
@@ -655,6 +667,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
+int g_pdl = 1;   // programmatic dependent launch on (zs_debug_set_pdl)
+
 cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, size_t smem, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
@@ -663,8 +677,17 @@ cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, 
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  zipgemm_kernel<<<grid, kGemmThreads, smem, stream>>>(p, xmap);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, zipgemm_kernel, p, xmap);
 }
 
 size_t gemm_smem_bytes(const GemmParams& p) {

@@ -59,6 +59,7 @@ struct GemmParams {
 };
 
 cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, size_t smem, cudaStream_t stream);
+extern int g_pdl;   // launch_gemm uses programmatic dependent launch when nonzero
 size_t gemm_smem_bytes(const GemmParams& p);
 int gemm_threads();
 int gemm_groups();

@@ -21,6 +21,8 @@ ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--cublas", action="store_true")
 ap.add_argument("--modes", default="auto", help="comma list of auto,fused,decoupled (forces the zs_gemm path)")
 ap.add_argument("--flags", default="0", help="comma list of zs_debug_set_flags values (timing experiments)")
+ap.add_argument("--graph-steps", type=int, default=1, help="GEMMs per captured graph (PDL needs >1)")
+ap.add_argument("--pdl", default="1", help="comma list of 0/1: programmatic dependent launch")
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -28,6 +30,7 @@ L = Z.lib()
 L.zs_debug_set_ring.argtypes = [ctypes.c_int]
 L.zs_debug_set_large_m.argtypes = [ctypes.c_longlong]
 L.zs_debug_set_flags.argtypes = [ctypes.c_int]
+L.zs_debug_set_pdl.argtypes = [ctypes.c_int]
 MODE_THR = {"auto": -1, "fused": 1 << 40, "decoupled": 0}
 
 
@@ -40,10 +43,12 @@ def timeit(fn, n_rot):
     with torch.cuda.stream(s):
         fn(0)
     torch.cuda.current_stream(dev).wait_stream(s)
+    S = a.graph_steps
     for i in range(n_rot):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            fn(i)
+            for j in range(S):
+                fn(i + j)
         gs.append(g)
     for i in range(10):
         gs[i % n_rot].replay()
@@ -54,7 +59,7 @@ def timeit(fn, n_rot):
         gs[i % n_rot].replay()
     e1.record()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) * 1e3 / a.iters
+    return e0.elapsed_time(e1) * 1e3 / (a.iters * a.graph_steps)
 
 
 for layer in a.layers.split(","):
@@ -71,16 +76,19 @@ for layer in a.layers.split(","):
     for M in [int(m) for m in a.ms.split(",")]:
         x = torch.randn((M, K), device=dev).to(torch.bfloat16)
         y = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
-        for mode, ring, fl in [(md, r, f) for md in a.modes.split(",")
-                               for r in ([int(r) for r in a.rings.split(",")] if a.rings else [0])
-                               for f in [int(f) for f in a.flags.split(",")]]:
+        for mode, ring, fl, pdl in [(md, r, f, pd) for md in a.modes.split(",")
+                                    for r in ([int(r) for r in a.rings.split(",")] if a.rings else [0])
+                                    for f in [int(f) for f in a.flags.split(",")]
+                                    for pd in [int(x) for x in a.pdl.split(",")]]:
             L.zs_debug_set_large_m(MODE_THR[mode])
             L.zs_debug_set_flags(fl)
+            L.zs_debug_set_pdl(pdl)
             ws = Z.workspace(M, N, K, dev)
             if ring:
                 L.zs_debug_set_ring(ring)
             us = timeit(lambda i: Z.gemm(x, comp[i % R], out=y, ws=ws), R)
-            rec = {"layer": layer, "M": M, "mode": mode, "ring": ring, "flags": fl, "us": round(us, 2),
+            rec = {"layer": layer, "M": M, "mode": mode, "ring": ring, "flags": fl, "pdl": pdl,
+                   "graph_steps": a.graph_steps, "us": round(us, 2),
                    "bits_per_el": round(zh.bits_per_element(), 3), "coverage": round(zh.covered / w.size, 4),
                    "tflops": round(2 * M * N * K / us / 1e6, 1),
                    "gbs": round((zh.nbytes() + 2 * M * K + 2 * M * N) / us / 1e3, 1)}
