@@ -570,8 +570,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               for (int qq = 0; qq < kRowBatch; ++qq) x ^= v[qq].x ^ v[qq].y ^ v[qq].z ^ v[qq].w;
               if (x == 0x9E3779B9u) p.counters[0] = x;   // keeps the decode live
             } else {
-#pragma unroll
-              for (int qq = 0; qq < kRowBatch; qq += 2) tmem_st8(taddr0 + 4u * (fb + qq), v[qq], v[qq + 1]);
+              tmem_st16(taddr0 + 4u * fb, v[0], v[1], v[2], v[3]);   // one 16-column store per 4 rows
             }
           }
           // publish the unit-quarter at once (the MMA warp spins on the slot's counter)
