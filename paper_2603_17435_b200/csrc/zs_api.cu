@@ -51,13 +51,20 @@ struct DevInfo {
 };
 
 zs_status device_check(int* sms) {
+  // per-device cache: the attribute queries cost several microseconds per call
+  static int cached_sms[64] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return ZS_ERR_UNSUPPORTED;
+  if (dev >= 0 && dev < 64 && cached_sms[dev] > 0) {
+    *sms = cached_sms[dev];
+    return ZS_OK;
+  }
   int major = 0, minor = 0, n = 0;
   if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return ZS_ERR_CUDA;
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   if (major != 10 || minor != 0) return ZS_ERR_UNSUPPORTED;  // built for sm_100a only
+  if (dev >= 0 && dev < 64) cached_sms[dev] = n;
   *sms = n;
   return ZS_OK;
 }
@@ -293,6 +300,14 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
     auto magic = [](uint32_t d) { return d <= 1u ? 0u : (uint32_t)((1ull << 32) / d + 1ull); };
     p.cdiv_magic = magic(p.n_cslots);
     p.adiv_magic = magic(p.n_aslots / (uint32_t)zs::gemm_units_per_stage());
+    // one-entry cache per host thread: repeated calls on the same activation buffer (the
+    // usual serving loop) skip the tensor-map encode
+    thread_local struct { const void* x; int64_t K, M, ldx; uint32_t box; CUtensorMap map; } xcache = {};
+    if (p.n_umma != cur_box && xcache.x == x && xcache.K == K && xcache.M == M && xcache.ldx == ldx &&
+        xcache.box == p.n_umma) {
+      xmap = xcache.map;
+      cur_box = p.n_umma;
+    }
     if (p.n_umma != cur_box) {
       cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
       cuuint64_t strides[1] = {(cuuint64_t)(ldx * 2)};
@@ -303,6 +318,7 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) return ZS_ERR_CUDA;
       cur_box = p.n_umma;
+      xcache.x = x; xcache.K = K; xcache.M = M; xcache.ldx = ldx; xcache.box = p.n_umma; xcache.map = xmap;
     }
     const int64_t grid = std::min<int64_t>(p.total_units, sms);
     cudaError_t e = zs::launch_gemm(p, xmap, (int)grid, zs::gemm_smem_bytes(p), (cudaStream_t)stream);

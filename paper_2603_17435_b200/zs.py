@@ -201,6 +201,10 @@ class ZsDevice:
                    + 16 * (self.sizes["n_blocktiles"] + 1))
 
     def c_struct(self) -> zs_tensor:
+        # the encoded tensors are immutable: build the ABI view once per ZsDevice
+        t = self.__dict__.get("_ct")
+        if t is not None:
+            return t
         t = zs_tensor()
         for f, _ in zs_sizes._fields_:
             setattr(t.sz, f, int(self.sizes[f]))
@@ -208,6 +212,7 @@ class ZsDevice:
         t.pad_word = self.pad_word
         t.b1, t.b2, t.b3 = self.b1.data_ptr(), self.b2.data_ptr(), self.b3.data_ptr()
         t.h, t.l, t.offsets = self.h.data_ptr(), self.l.data_ptr(), self.offsets.data_ptr()
+        self.__dict__["_ct"] = t
         return t
 
 
