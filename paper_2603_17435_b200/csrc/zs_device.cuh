@@ -272,103 +272,14 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(uint32_t M, uint32_t N) {
 // data-dependent branch on the common path.  Rows with >= 3 fallback
 // elements (rank >= 2) take a short patch loop (~0.05% of rows at r = 0.98).
 //
-// lut[m] (uint4): for output word j (elements 2j, 2j+1):
+// Selector table entry lut[m] (csrc/zs_lut.h, generated by scripts/gen_lut.py), m = the
+// row's spatial-indicator byte; for output word j (elements 2j, 2j+1):
 //   bits  0..15  PRMT selector that pulls the H byte of element 2j into byte 0 and its
 //                sign-replicated copy into byte 1, likewise element 2j+1 into bytes 2, 3
 //   bits 16..31  PRMT selector over {Lpair, assembled word}: fallback elements of rank 0/1
 //                take L bytes (0,1)/(2,3), in-window elements keep their assembled half.
-__device__ __forceinline__ uint4 build_lut_entry(uint32_t m) {
-  uint32_t e[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint32_t hs = 0, fs = 0;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int i = 2 * j + h;
-      const uint32_t pre = __popc(m & ((1u << i) - 1u));  // set bits below i
-      const uint32_t rank = (uint32_t)i - pre;              // fallback rank of element i
-      hs |= (pre | ((pre | 8u) << 4)) << (8 * h);
-      uint32_t f;
-      if ((m >> i) & 1u)
-        f = (4u + 2u * h) | ((5u + 2u * h) << 4);  // keep assembled halfword h
-      else if (rank == 0)
-        f = 0u | (1u << 4);
-      else
-        f = 2u | (3u << 4);                         // rank 1 (rank >= 2 is patched)
-      fs |= f << (8 * h);
-    }
-    e[j] = hs | (fs << 16);
-  }
-  // bit 7 (sign-replicate of the high-byte selector of element 0; copy and replicate give
-  // the same bit 15) flags rows with >= 3 fallbacks
-  e[0] &= ~0x80u;
-  if (__popc(m) < 6) e[0] |= 0x80u;
-  return make_uint4(e[0], e[1], e[2], e[3]);
-}
-
-// Decode one FragTile row.
-//   p1..p3   : the 64-bit bit-planes of the FragTile (lo/hi halves)
-//   r8       : row inside the FragTile (0..7) -> byte r8 of every plane
-//   H        : byte pointer to the BlockTile's PackedSignMantissa segment (smem)
-//   hs       : H index of the row's first in-window element (prefix popcount)
-//   L        : BlockTile's FullValue segment (smem); ls: L index of its first fallback
-//   eb7x2    : ((e_base mod 256) << 7) replicated in both halfwords
-// Returns 8 bf16 (element c in halfword c of the uint4, i.e. K order).
-__device__ __forceinline__ uint4 decode_row(uint64_t p1, uint64_t p2, uint64_t p3, uint32_t r8,
-                                            const uint8_t* __restrict__ H, uint32_t hs,
-                                            const uint16_t* __restrict__ L, uint32_t ls, const uint4* lut,
-                                            uint32_t eb7x2) {
-  const uint32_t sh = 8u * r8;
-  const uint32_t b1 = (uint32_t)(p1 >> sh) & 0xFFu;
-  const uint32_t b2 = (uint32_t)(p2 >> sh) & 0xFFu;
-  const uint32_t b3 = (uint32_t)(p3 >> sh) & 0xFFu;
-  const uint32_t m = b1 | b2 | b3;  // spatial indicator of the row
-  const uint4 ent = lut[m];
-
-  // 8 H bytes starting at hs (byte-granular window from three aligned words)
-  const uint32_t* H32 = reinterpret_cast<const uint32_t*>(H) + (hs >> 2);
-  const uint32_t hsh = (hs & 3u) * 8u;
-  const uint32_t w0 = H32[0], w1 = H32[1], w2 = H32[2];
-  const uint32_t hlo = __funnelshift_r(w0, w1, hsh);
-  const uint32_t hhi = __funnelshift_r(w1, w2, hsh);
-
-  // first two fallback values of the row
-  const uint32_t* L32 = reinterpret_cast<const uint32_t*>(L) + (ls >> 1);
-  const uint32_t lpair = __funnelshift_r(L32[0], L32[1], (ls & 1u) * 16u);
-
-  // codewords c_i = b3_i b2_i b1_i, two per 32-bit word (halfword h = element 2j+h)
-  uint32_t out[4];
-  const uint32_t sel[4] = {ent.x, ent.y, ent.z, ent.w};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t c0 = ((b1 >> (2 * j)) & 1u) | (((b2 >> (2 * j)) & 1u) << 1) | (((b3 >> (2 * j)) & 1u) << 2);
-    const uint32_t c1 =
-        ((b1 >> (2 * j + 1)) & 1u) | (((b2 >> (2 * j + 1)) & 1u) << 1) | (((b3 >> (2 * j + 1)) & 1u) << 2);
-    const uint32_t E = (c0 | (c1 << 16)) * 128u + eb7x2;        // (e_base + c) << 7 per half
-    const uint32_t P = __byte_perm(hlo, hhi, sel[j] & 0xFFFFu);  // s,s.. | mantissa bytes
-    const uint32_t asm_w = (P & 0x807F807Fu) | (E & 0x7F807F80u);
-    out[j] = __byte_perm(lpair, asm_w, sel[j] >> 16);
-  }
-
-  // rank >= 2 fallbacks (rare): patch from L directly
-  if (__popc(m) < 6) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t pre = __popc(m & ((1u << i) - 1u));
-      const uint32_t rank = (uint32_t)i - pre;
-      if (!((m >> i) & 1u) && rank >= 2) {
-        const uint32_t v = L[ls + rank];
-        const int j = i >> 1;
-        if (i & 1)
-          out[j] = (out[j] & 0x0000FFFFu) | (v << 16);
-        else
-          out[j] = (out[j] & 0xFFFF0000u) | v;
-      }
-    }
-  }
-  return make_uint4(out[0], out[1], out[2], out[3]);
-}
-
+// Bit 7 of word 0 (a sign-replicate bit whose two modes give the same result) flags rows
+// with >= 3 fallbacks, which take the rare patch path.
 
 // ------------------------------------------------------------------ row decoder, v2
 // Same contract as decode_row, restructured for the sm_100a issue budget:

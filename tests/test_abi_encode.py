@@ -150,3 +150,20 @@ def test_gemm_path_and_workspace_sizes(Z):
     assert L.zs_gemm_workspace_bytes(0, N, K) == 0
     # K is padded to a multiple of 8 elements (16-B rows of the decoded operand)
     assert L.zs_gemm_workspace_bytes(large + 1, 100, 1001) >= 2 * 100 * 1008
+
+
+def test_selector_table_matches_generator():
+    # csrc/zs_lut.h must be exactly what scripts/gen_lut.py derives from the rank definition
+    # (Alg. 2: idx_H = popc(M & ((1 << p) - 1)), fallback rank p - idx_H)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("gen_lut", os.path.join(ROOT, "scripts", "gen_lut.py"))
+    gl = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gl)
+    src = open(os.path.join(ROOT, "paper_2603_17435_b200", "csrc", "zs_lut.h")).read()
+    rows = re.findall(r"\{0x([0-9A-F]{8})u, 0x([0-9A-F]{8})u, 0x([0-9A-F]{8})u, 0x([0-9A-F]{8})u\}", src)
+    assert len(rows) == 256
+    for m, r in enumerate(rows):
+        assert [int(v, 16) for v in r] == gl.entry(m)
+    # spot-check the rank semantics: m = 0b10110101 -> element 2 is in-window with H rank 1
+    e = gl.entry(0b10110101)
+    assert (e[1] & 0xF) == 1                      # word 1, low byte <- H byte of rank 1
