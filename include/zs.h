@@ -10,6 +10,9 @@
  *                    using the decode of Alg. 2                     [device]
  *   zs_gemm          ZipGEMM: Y = X * W^T with W streamed compressed and decoded per
  *                    tile inside the kernel (north star)             [device]
+ *   zs_gemm_peer     column-sharded ZipGEMM whose epilogue also stores into every
+ *                    rank's Y over NVLink and signals flags    [device]
+ *   zs_peer_wait     stream wait for those flags                                [device]
  *
  * Notation: the paper writes Y = W X with W (M out x K) and X (K x N tokens).
  * This ABI uses the F.linear convention: X is [M tokens][K], W is [N out][K], Y is [M][N].
@@ -155,6 +158,66 @@ int zs_gemm_is_decoupled(int64_t M, int64_t N, int64_t K);
 zs_status zs_gemm(const uint16_t *x, int64_t ldx, const zs_tensor *w, uint16_t *y, int64_t ldy,
                   int64_t M, int64_t N, int64_t K, void *workspace, size_t workspace_bytes,
                   void *stream);
+
+/* ---------------------------------------------------------------- output exchange (f2)
+ * Column-sharded ZipGEMM (north star) with the all-gather of the Y slices fused
+ * into the GEMM (the paper leaves multi-GPU to the serving layer).
+ * Rank r of `world` holds the W rows [col0, col0 + N) (a contiguous byte range of the
+ * encoding, dist.shard_rows) and a full output Y_r [M][ldy].  zs_gemm_peer computes its
+ * slice and STORES EVERY ELEMENT INTO ALL RANKS' Y (the epilogue writes the local copy and
+ * the peers' copies through peer pointers over NVLink), then, once the whole grid's stores
+ * are visible at system scope, writes `epoch` to flags[r][rank] for every r.  zs_peer_wait
+ * on rank r then blocks its stream until flags[r][0..world) all reached `epoch`, after
+ * which Y_r holds the full product.  No collective library call, no permute.
+ *
+ *   y[r], flags[r]: device pointers valid in the calling process -- the caller's own
+ *     buffers for r == rank, CUDA-IPC-mapped (zs_ipc_open) or same-device buffers otherwise.
+ *     flags[r] has `world` u32 words.  Caller-owned; the library keeps no state.
+ *   epoch: a value the flags have not held since the previous wait (e.g. a step counter;
+ *     the wait compares wrap-safely, flag - epoch >= 0 as int32).
+ *   Reuse: the caller must not start a step that writes Y_r while rank r may still read
+ *     the previous contents (double-buffer Y by epoch parity, or a barrier).
+ * Large M (zs_gemm_is_decoupled): cuBLAS writes the local slice, then one copy kernel
+ * broadcasts it and signals.  workspace: zs_gemm_peer_workspace_bytes = 256 B holding the
+ * signalling launch's CTA counter, then zs_gemm's workspace; zero-filled once before first
+ * use (the counter is self-cleaning; the rest follows zs_gemm_workspace_bytes). */
+#define ZS_MAX_PEERS 8
+#define ZS_IPC_HANDLE_BYTES 64
+#define ZS_PEER_WAIT_TIMEOUT_NS 20000000000ull   /* zs_peer_wait traps after 20 s */
+
+typedef struct {
+    int32_t world;                    /* 1..ZS_MAX_PEERS                                  */
+    int32_t rank;                     /* 0..world-1                                       */
+    uint16_t *y[ZS_MAX_PEERS];        /* rank r's full Y [M][ldy] BF16 (device pointers)  */
+    int64_t ldy;                      /* elements, >= col0 + N, the same on every rank    */
+    int64_t col0;                     /* first Y column of this rank's slice              */
+    uint32_t *flags[ZS_MAX_PEERS];    /* rank r's flag array, `world` u32 words           */
+    uint32_t epoch;                   /* written to flags[r][rank] when the slice landed  */
+} zs_peer_out;
+
+size_t zs_gemm_peer_workspace_bytes(int64_t M, int64_t N, int64_t K);
+
+/* Y_r[:, col0:col0+N] = X W^T for every rank r (see above).  x, w, M, N, K as zs_gemm (N =
+ * this rank's shard rows).  Errors: as zs_gemm, plus ZS_ERR_INVALID_ARG (world / rank out
+ * of range, null y[r] or flags[r]) and ZS_ERR_SHAPE (ldy < col0 + N). */
+zs_status zs_gemm_peer(const uint16_t *x, int64_t ldx, const zs_tensor *w, const zs_peer_out *out,
+                       int64_t M, int64_t N, int64_t K, void *workspace, size_t workspace_bytes,
+                       void *stream);
+
+/* Blocks `stream` until flags[0..world) (this rank's flag array, device memory) all reached
+ * epoch (one 32-thread launch, acquire loads at system scope).  A flag that does not arrive
+ * within ZS_PEER_WAIT_TIMEOUT_NS traps the kernel (the stream reports a launch failure)
+ * instead of hanging.  Errors: ZS_ERR_INVALID_ARG, ZS_ERR_UNSUPPORTED, ZS_ERR_CUDA. */
+zs_status zs_peer_wait(const uint32_t *flags, int32_t world, uint32_t epoch, void *stream);
+
+/* CUDA IPC plumbing for zs_peer_out (host calls).  zs_ipc_get_handle: the handle
+ * (ZS_IPC_HANDLE_BYTES opaque bytes) of the allocation holding dev_ptr and dev_ptr's byte
+ * offset inside it.  zs_ipc_open (in ANOTHER process): map it; *base + offset is the peer's
+ * dev_ptr.  zs_ipc_close: unmap.  Errors: ZS_ERR_INVALID_ARG, ZS_ERR_UNSUPPORTED, ZS_ERR_CUDA
+ * (including opening a handle in the process that created it). */
+zs_status zs_ipc_get_handle(const void *dev_ptr, void *handle, int64_t *offset);
+zs_status zs_ipc_open(const void *handle, void **base);
+zs_status zs_ipc_close(void *base);
 
 /* GPU-side encoder: the same bytes as zs_encode_measure / zs_encode (Alg. 1,
  * P:306-333; canonical order S:277), computed on the device from a DEVICE matrix w (row-major,

@@ -14,7 +14,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libzs.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CU_SOURCES = ["zs_api.cu", "zs_decompress.cu", "zs_gemm.cu", "zs_encode_gpu.cu"]
+CU_SOURCES = ["zs_api.cu", "zs_decompress.cu", "zs_gemm.cu", "zs_encode_gpu.cu", "zs_peer.cu"]
 CPP_SOURCES = ["zs_encode.cpp"]
 HEADERS = ["zs_device.cuh", "zs_kernels.h", "zs_host.h", "zs_lut.h"]
 

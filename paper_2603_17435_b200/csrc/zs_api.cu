@@ -107,6 +107,19 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_tiled() {
   return fn;
 }
 
+PFN_cuMemGetAddressRange_v3020 get_addr_range() {
+  static PFN_cuMemGetAddressRange_v3020 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(p);
+  });
+  return fn;
+}
+
 }  // namespace
 
 extern "C" const char* zs_status_string(zs_status s) {
@@ -191,8 +204,18 @@ extern "C" size_t zs_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
 
 extern "C" int zs_gemm_is_decoupled(int64_t M, int64_t N, int64_t K) { return use_decoupled(M, N, K) ? 1 : 0; }
 
-extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w, uint16_t* y, int64_t ldy, int64_t M,
-                             int64_t N, int64_t K, void* workspace, size_t workspace_bytes, void* stream) {
+// fused output exchange (f2) of zs_gemm_peer: extra output copies and the flags to signal
+struct PeerSetup {
+  uint16_t* ypeer[zs::kMaxPeers];
+  uint32_t* flag[zs::kMaxPeers];
+  uint32_t* done;
+  int npeer, nflag;
+  uint32_t epoch;
+};
+
+static zs_status gemm_core(const uint16_t* x, int64_t ldx, const zs_tensor* w, uint16_t* y, int64_t ldy, int64_t M,
+                           int64_t N, int64_t K, void* workspace, size_t workspace_bytes, void* stream,
+                           const PeerSetup* ps) {
   g_last_launches = 0;
   zs_status st = validate_tensor(w);
   if (st != ZS_OK) return st;
@@ -224,6 +247,22 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
                                      (int)ldy, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
     if (bs != CUBLAS_STATUS_SUCCESS) return ZS_ERR_CUDA;
     g_last_launches = 1;   // our kernels only (the cuBLAS GEMM is library code)
+    if (ps) {
+      // broadcast the slice cuBLAS wrote to the peers' Y, then signal (one launch)
+      zs::PeerCopyParams cp{};
+      cp.src = y;
+      for (int i = 0; i < ps->npeer; ++i) cp.dst[i] = ps->ypeer[i];
+      for (int i = 0; i < ps->nflag; ++i) cp.flag[i] = ps->flag[i];
+      cp.done = ps->done;
+      cp.rows = M;
+      cp.cols = N;
+      cp.ld = ldy;
+      cp.npeer = ps->npeer;
+      cp.nflag = ps->nflag;
+      cp.epoch = ps->epoch;
+      if (zs::launch_peer_copy(cp, sms, (cudaStream_t)stream) != cudaSuccess) return ZS_ERR_CUDA;
+      g_last_launches = 2;
+    }
     return ZS_OK;
   }
 
@@ -320,12 +359,103 @@ extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w,
       cur_box = p.n_umma;
       xcache.x = x; xcache.K = K; xcache.M = M; xcache.ldx = ldx; xcache.box = p.n_umma; xcache.map = xmap;
     }
+    if (ps) {
+      // every chunk stores to the peers; only the last one signals (chunks are stream-ordered)
+      for (int i = 0; i < ps->npeer; ++i) p.ypeer[i] = ps->ypeer[i];
+      for (int i = 0; i < ps->nflag; ++i) p.flag[i] = ps->flag[i];
+      p.npeer = ps->npeer;
+      p.nflag = ps->nflag;
+      p.epoch = ps->epoch;
+      p.done = (m0 + chunk >= M) ? ps->done : nullptr;
+    }
     const int64_t grid = std::min<int64_t>(p.total_units, sms);
     cudaError_t e = zs::launch_gemm(p, xmap, (int)grid, zs::gemm_smem_bytes(p), (cudaStream_t)stream);
     if (e != cudaSuccess) return ZS_ERR_CUDA;
     ++launches;
   }
   g_last_launches = launches;
+  return ZS_OK;
+}
+
+extern "C" zs_status zs_gemm(const uint16_t* x, int64_t ldx, const zs_tensor* w, uint16_t* y, int64_t ldy, int64_t M,
+                             int64_t N, int64_t K, void* workspace, size_t workspace_bytes, void* stream) {
+  return gemm_core(x, ldx, w, y, ldy, M, N, K, workspace, workspace_bytes, stream, nullptr);
+}
+
+// ------------------------------------------------------------------ output exchange (f2)
+extern "C" size_t zs_gemm_peer_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+  const size_t b = zs_gemm_workspace_bytes(M, N, K);
+  return b ? b + 256 : 0;   // + the CTA completion counter of the signalling launch (first 256 B)
+}
+
+extern "C" zs_status zs_gemm_peer(const uint16_t* x, int64_t ldx, const zs_tensor* w, const zs_peer_out* out,
+                                  int64_t M, int64_t N, int64_t K, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
+  g_last_launches = 0;
+  if (!out) return ZS_ERR_INVALID_ARG;
+  const int world = out->world, rank = out->rank;
+  if (world < 1 || world > ZS_MAX_PEERS || rank < 0 || rank >= world) return ZS_ERR_INVALID_ARG;
+  for (int r = 0; r < world; ++r)
+    if (!out->y[r] || !out->flags[r]) return ZS_ERR_INVALID_ARG;
+  if (out->col0 < 0 || N < 1 || out->ldy < out->col0 + N) return ZS_ERR_SHAPE;
+  if (!workspace || workspace_bytes < zs_gemm_peer_workspace_bytes(M, N, K)) return ZS_ERR_CAPACITY;
+  const size_t base = zs_gemm_workspace_bytes(M, N, K);
+  PeerSetup ps{};
+  for (int r = 0; r < world; ++r) {
+    if (r != rank) ps.ypeer[ps.npeer++] = out->y[r] + out->col0;
+    ps.flag[ps.nflag++] = out->flags[r] + rank;
+  }
+  // the counter leads the workspace, so the decoupled path's (dirty) scratch never covers it
+  ps.done = reinterpret_cast<uint32_t*>(workspace);
+  ps.epoch = out->epoch;
+  return gemm_core(x, ldx, w, out->y[rank] + out->col0, out->ldy, M, N, K,
+                   reinterpret_cast<uint8_t*>(workspace) + 256, base, stream, &ps);
+}
+
+extern "C" zs_status zs_peer_wait(const uint32_t* flags, int32_t world, uint32_t epoch, void* stream) {
+  g_last_launches = 0;
+  if (!flags || world < 1 || world > ZS_MAX_PEERS) return ZS_ERR_INVALID_ARG;
+  int sms = 0;
+  zs_status st = device_check(&sms);
+  if (st != ZS_OK) return st;
+  if (zs::launch_peer_wait(flags, world, epoch, ZS_PEER_WAIT_TIMEOUT_NS, (cudaStream_t)stream) != cudaSuccess)
+    return ZS_ERR_CUDA;
+  g_last_launches = 1;
+  return ZS_OK;
+}
+
+extern "C" zs_status zs_ipc_get_handle(const void* dev_ptr, void* handle, int64_t* offset) {
+  if (!dev_ptr || !handle || !offset) return ZS_ERR_INVALID_ARG;
+  auto range = get_addr_range();
+  if (!range) return ZS_ERR_UNSUPPORTED;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS) return ZS_ERR_INVALID_ARG;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)) != cudaSuccess) return ZS_ERR_CUDA;
+  static_assert(sizeof(h) == ZS_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle, &h, sizeof(h));
+  *offset = (int64_t)((CUdeviceptr)dev_ptr - base);
+  return ZS_OK;
+}
+
+extern "C" zs_status zs_ipc_open(const void* handle, void** base) {
+  if (!handle || !base) return ZS_ERR_INVALID_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  if (cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    return ZS_ERR_CUDA;
+  }
+  return ZS_OK;
+}
+
+extern "C" zs_status zs_ipc_close(void* base) {
+  if (!base) return ZS_ERR_INVALID_ARG;
+  if (cudaIpcCloseMemHandle(base) != cudaSuccess) {
+    cudaGetLastError();
+    return ZS_ERR_CUDA;
+  }
   return ZS_OK;
 }
 

@@ -115,6 +115,62 @@ __device__ __forceinline__ uint32_t ld_acquire_shared(const uint32_t* p) {
   return v;
 }
 
+// system-scope flag hand-off between GPUs (peer memory over NVLink, or CUDA-IPC-mapped
+// memory of another process): release store / acquire load of a global u32
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// CTA-completion counter of the exchange: release orders this CTA's output stores (made
+// visible to this thread by the preceding CTA barrier; release is cumulative) before the
+// increment; acquire lets the last arriver's flag release cover every CTA's stores
+__device__ __forceinline__ uint32_t atom_add_acq_rel_sys(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.sys.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Completion signal of the fused exchange, called by one full warp of every CTA after a
+// CTA barrier that follows all of the CTA's output stores.  Lane 0 counts the CTA in with
+// a GPU-scope release (cumulative over the CTA's stores; every CTA is on this GPU, so the
+// counter needs no system scope); the warp of the CTA that arrives last (its acquire
+// sees every CTA's release) resets the counter and stores `epoch` to the nflag flags,
+// lane i -> flag[i], as ONE warp-wide system-scope release: causality order is
+// transitive, so a peer that acquires a flag sees every CTA's stores (one system fence
+// per launch instead of one per CTA and flag).
+__device__ __forceinline__ void signal_peers(uint32_t* done, uint32_t* const* flag, int nflag, uint32_t epoch,
+                                             int lane) {
+  uint32_t old = 0;
+  if (lane == 0) old = atom_add_acq_rel_gpu(done, 1u);
+  old = __shfl_sync(0xFFFFFFFFu, old, 0);
+  if (old != gridDim.x - 1) return;
+  if (lane == 0) *done = 0u;   // self-cleaning for the next call
+  __syncwarp();                // lane 0's acquire happens before the other lanes' releases
+  uint32_t* f = nullptr;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (i == lane && i < nflag) f = flag[i];
+  if (f) st_release_sys(f, epoch);
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // generic-proxy smem writes -> visible to the async proxy (tcgen05.mma operand reads)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -142,8 +142,31 @@ __device__ __forceinline__ void wait_count(const uint32_t* ctr, uint32_t need) {
   }
 }
 
+// fused exchange (f2): copy the mc outputs of one weight row n (column of Y), just stored
+// to the local Y by this thread, into every peer's Y.  Out of line, so the exchange adds no
+// register pressure to the rest of the kernel (it shares one 64-register allocation).
+// Loads go out 16 at a time (independent L2 round trips), then every peer gets the batch.
+__device__ __noinline__ void copy_to_peers(uint16_t* const* ypeer, int npeer, const uint16_t* y, int64_t ldy,
+                                           int64_t off, int mc) {
+  for (int m0 = 0; m0 < mc; m0 += 16, off += 16 * ldy) {
+    uint16_t v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (m0 + j < mc) v[j] = y[off + j * ldy];
+    for (int i = 0; i < npeer; ++i) {
+      uint16_t* d = ypeer[i];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (m0 + j < mc) d[off + j * ldy] = v[j];
+    }
+  }
+}
+
+// kPeer: the fused output exchange (peer stores + completion signal) is compiled in; the
+// plain instance is the single-GPU kernel with no extra registers or branches
+template <bool kPeer>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    zipgemm_kernel(const GemmParams p, const __grid_constant__ CUtensorMap xmap) {
+    zipgemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment for the SW128 X tiles
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -624,6 +647,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bars->accempty[seg & 1]);
+      if (kPeer && full && nvalid && p.npeer > 0)
+        copy_to_peers(p.ypeer, p.npeer, p.y, p.ldy, (int64_t)p.m0 * p.ldy + n, p.mc);
       if (!full) {
         __threadfence();
         named_bar_sync(1, 128);
@@ -651,10 +676,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               }
             }
           }
+          if (kPeer && nvalid && p.npeer > 0)
+            copy_to_peers(p.ypeer, p.npeer, p.y, p.ldy, (int64_t)p.m0 * p.ldy + n, p.mc);
           if (et == 0) p.counters[band] = 0u;
         }
         named_bar_sync(1, 128);
       }
+    }
+    if (kPeer && p.done) {
+      // fused exchange (f2): this CTA's Y stores (local and peer) happen before its
+      // arrival; the CTA that arrives last then releases the flags, so a peer that
+      // acquires flag == epoch sees every tile of this rank's slice
+      named_bar_sync(1, 128);   // the 128 epilogue threads' stores happen before et 0's release
+      if (et < 32) signal_peers(p.done, p.flag, p.nflag, p.epoch, lane);
     }
   }
 
@@ -672,7 +706,9 @@ cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, 
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e =
-        cudaFuncSetAttribute(zipgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(zipgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(zipgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -686,7 +722,8 @@ cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, 
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, zipgemm_kernel, p, xmap);
+  if (p.npeer > 0 || p.nflag > 0 || (p.dbg & 0x100u)) return cudaLaunchKernelEx(&cfg, zipgemm_kernel<true>, p, xmap);
+  return cudaLaunchKernelEx(&cfg, zipgemm_kernel<false>, p, xmap);
 }
 
 size_t gemm_smem_bytes(const GemmParams& p) {

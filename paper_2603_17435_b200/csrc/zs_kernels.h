@@ -28,6 +28,8 @@ cudaError_t launch_decompress(const DecompParams& p, int grid, int warps, size_t
 size_t decompress_smem_bytes(uint32_t stage_bytes, int warps);
 int decompress_max_warps();
 
+constexpr int kMaxPeers = 8;   // ZS_MAX_PEERS
+
 struct GemmParams {
   const uint64_t* b1;
   const uint64_t* b2;
@@ -56,7 +58,32 @@ struct GemmParams {
   uint32_t cdiv_magic, adiv_magic;  // fastdiv multipliers of n_cslots / n_aslots
   unsigned long long* trace;  // optional per-unit event timestamps (debug; nullptr = off)
   uint32_t dbg;               // debug experiment flags (0 in production; zs_debug_set_flags)
+  // fused output exchange: every Y element is also stored to ypeer[i]
+  // (same [m][n] addressing and ldy as y), and once all CTAs' stores are visible the last
+  // CTA writes `epoch` to flag[0..nflag) (system scope).  npeer = nflag = 0: plain GEMM.
+  uint16_t* ypeer[kMaxPeers];
+  uint32_t* flag[kMaxPeers];
+  uint32_t* done;             // CTA completion counter (zero between calls), nullptr = no signal
+  int32_t npeer, nflag;
+  uint32_t epoch;
 };
+
+// Copy a [rows][cols] BF16 slice (leading dimension ld) from src to each of npeer
+// destinations (same addressing), then -- after every CTA's stores are visible at system
+// scope -- write `epoch` to flag[0..nflag).  `done`: zeroed counter, left zeroed.
+struct PeerCopyParams {
+  const uint16_t* src;
+  uint16_t* dst[kMaxPeers];
+  uint32_t* flag[kMaxPeers];
+  uint32_t* done;
+  int64_t rows, cols, ld;
+  int32_t npeer, nflag;
+  uint32_t epoch;
+};
+cudaError_t launch_peer_copy(const PeerCopyParams& p, int sms, cudaStream_t s);
+// Spin (one thread per flag, ld.acquire.sys) until flags[0..n) have all reached `epoch`
+// (wrap-safe comparison); traps after timeout_ns so a missing peer cannot hang the GPU.
+cudaError_t launch_peer_wait(const uint32_t* flags, int n, uint32_t epoch, uint64_t timeout_ns, cudaStream_t s);
 
 cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, size_t smem, cudaStream_t stream);
 extern int g_pdl;   // launch_gemm uses programmatic dependent launch when nonzero

@@ -6,6 +6,11 @@ contiguous byte range of B1/B2/B3/H/L; the shard keeps the full matrix's e_base 
 C3), so 1-GPU and w-GPU runs decode identical bytes.  Each rank runs zs_gemm on its shard
 with the replicated X and the slices Y_r [M][N/w] are all-gathered (NCCL over NVLink on
 the GPU box; gloo in the CPU tests) and permuted to Y [M][N].
+
+exchange="peer" replaces the all-gather: every rank maps every other
+rank's Y buffers and flag array through CUDA IPC (handles exchanged over the process group),
+zs_gemm_peer stores the slice into all ranks' Y from the GEMM epilogue and signals, and
+zs_peer_wait blocks the stream until every rank's slice has landed.
 """
 from __future__ import annotations
 
@@ -58,21 +63,93 @@ def gather_columns(y_local, world: int, group=None):
     return buf.permute(1, 0, 2).reshape(M, world * nw)
 
 
-class ShardedZipLinear:
-    """Y = X W^T with W column-sharded over the ranks of the default process group."""
+def peer_tables(rank: int, world: int, local_addrs, all_handles, open_fn):
+    """Address tables of the fused exchange from the all-gathered IPC handles (host logic).
 
-    def __init__(self, zh_full: ZsHost, rank: int, world: int, device):
+    local_addrs: this rank's own buffer addresses (one per exchanged buffer).
+    all_handles[r][j] = (handle bytes, byte offset) of rank r's buffer j.
+    open_fn(handle) -> base address in this process; called once per distinct handle of
+    another rank (buffers sharing an allocation share its mapping).
+    Returns (tables[j][r] = address of rank r's buffer j in this process, opened bases).
+    """
+    assert len(all_handles) == world
+    nbuf = len(local_addrs)
+    opened = {}
+    tables = [[0] * world for _ in range(nbuf)]
+    for r in range(world):
+        assert len(all_handles[r]) == nbuf
+        for j, (h, off) in enumerate(all_handles[r]):
+            if r == rank:
+                tables[j][r] = local_addrs[j]
+                continue
+            if h not in opened:
+                opened[h] = open_fn(h)
+            tables[j][r] = opened[h] + off
+    return tables, list(opened.values())
+
+
+class PeerOutputs:
+    """The symmetric output buffers of the fused exchange: on every rank, `nbuf` full outputs
+    Y [M][N] (double-buffered by step parity, so a rank that runs ahead never overwrites an
+    output a slower rank may still read) and one flag array [world] u32, mapped into every
+    other rank's address space by CUDA IPC."""
+
+    def __init__(self, M: int, N: int, rank: int, world: int, device, group=None, nbuf: int = 2):
+        import torch
+        import torch.distributed as dist
+        from . import zs as Z
+        self.rank, self.world, self.M, self.N = rank, world, M, N
+        self.y = [torch.zeros((M, N), dtype=torch.bfloat16, device=device) for _ in range(nbuf)]
+        self.flags = torch.zeros(world, dtype=torch.int32, device=device)
+        mine = [Z.ipc_handle(t) for t in self.y + [self.flags]]
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        local = [t.data_ptr() for t in self.y + [self.flags]]
+        tables, self._opened = peer_tables(rank, world, local, allh, Z.ipc_open)
+        self.y_tables, self.flag_table = tables[:nbuf], tables[nbuf]
+        dist.barrier(group=group)
+
+    def close(self):
+        from . import zs as Z
+        for b in self._opened:
+            Z.ipc_close(b)
+        self._opened = []
+
+
+class ShardedZipLinear:
+    """Y = X W^T with W column-sharded over the ranks of the default process group.
+
+    exchange="nccl": zs_gemm on the shard, all_gather_into_tensor + permute.
+    exchange="peer": zs_gemm_peer (epilogue stores into every rank's Y over NVLink, flags)
+    + zs_peer_wait; M is fixed at construction (the exchanged buffers are [M][N])."""
+
+    def __init__(self, zh_full: ZsHost, rank: int, world: int, device, exchange: str = "nccl", M: int | None = None,
+                 group=None):
         self.rank, self.world = rank, world
         self.r0, self.r1 = shard_bounds(zh_full.rows, world, rank)
         widths = {shard_bounds(zh_full.rows, world, r)[1] - shard_bounds(zh_full.rows, world, r)[0]
                   for r in range(world)}
-        assert len(widths) == 1, "all-gather needs equal shard widths"
+        assert exchange == "peer" or len(widths) == 1, "the all-gather needs equal shard widths"
         self.host = shard_rows(zh_full, self.r0, self.r1)
         self.dev = self.host.to(device)
         self.N = zh_full.rows
+        self.exchange = exchange
+        self.step = 0
+        if exchange == "peer":
+            assert M is not None, "exchange='peer' needs M"
+            self.peer = PeerOutputs(M, self.N, rank, world, device, group=group)
+        else:
+            assert exchange == "nccl", exchange
 
     def __call__(self, x):
-        from .zs import gemm
+        from .zs import gemm, gemm_peer, peer_wait
+        if self.exchange == "peer":
+            self.step += 1
+            b = self.step % len(self.peer.y)
+            gemm_peer(x, self.dev, self.peer.y_tables[b], self.peer.flag_table, self.rank, self.r0, self.step,
+                      ldy=self.N)
+            peer_wait(self.peer.flags, self.world, self.step)
+            return self.peer.y[b]
         y_local = gemm(x, self.dev)
         if self.world == 1:
             return y_local

@@ -21,7 +21,12 @@ ZS_STATUS = {0: "ZS_OK", 1: "ZS_ERR_INVALID_ARG", 2: "ZS_ERR_SHAPE", 3: "ZS_ERR_
 # every symbol include/zs.h declares (checked by tests/test_abi.py)
 EXPORTS = ["zs_encode_bound", "zs_encode_measure", "zs_encode", "zs_decompress", "zs_gemm_workspace_bytes",
            "zs_gemm_is_decoupled", "zs_gemm", "zs_last_launch_count", "zs_status_string",
-           "zs_encode_device_workspace_bytes", "zs_encode_measure_device", "zs_encode_device"]
+           "zs_encode_device_workspace_bytes", "zs_encode_measure_device", "zs_encode_device",
+           "zs_gemm_peer_workspace_bytes", "zs_gemm_peer", "zs_peer_wait", "zs_ipc_get_handle", "zs_ipc_open",
+           "zs_ipc_close"]
+
+MAX_PEERS = 8            # ZS_MAX_PEERS
+IPC_HANDLE_BYTES = 64    # ZS_IPC_HANDLE_BYTES
 
 
 class ZsError(RuntimeError):
@@ -41,6 +46,12 @@ class zs_tensor(ctypes.Structure):
                 ("reserved", ctypes.c_uint16),
                 ("b1", ctypes.c_void_p), ("b2", ctypes.c_void_p), ("b3", ctypes.c_void_p),
                 ("h", ctypes.c_void_p), ("l", ctypes.c_void_p), ("offsets", ctypes.c_void_p)]
+
+
+class zs_peer_out(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("y", ctypes.c_void_p * MAX_PEERS),
+                ("ldy", ctypes.c_int64), ("col0", ctypes.c_int64), ("flags", ctypes.c_void_p * MAX_PEERS),
+                ("epoch", ctypes.c_uint32)]
 
 
 _lib = None
@@ -74,8 +85,21 @@ def lib():
         L.zs_encode_device.argtypes = [vp, i64, i64, i64, i32, ctypes.POINTER(zs_sizes), vp, vp, vp, vp, vp, vp,
                                        ctypes.POINTER(zs_sizes), ctypes.POINTER(ctypes.c_uint16), vp, ctypes.c_size_t,
                                        vp]
+        if not hasattr(L, "zs_gemm_peer"):   # an older debug build (ZS_LIB): no exchange entry points
+            L.zs_last_launch_count.restype = ctypes.c_int
+            _lib = L
+            return L
+        L.zs_gemm_peer_workspace_bytes.argtypes = [i64, i64, i64]
+        L.zs_gemm_peer_workspace_bytes.restype = ctypes.c_size_t
+        L.zs_gemm_peer.argtypes = [vp, i64, ctypes.POINTER(zs_tensor), ctypes.POINTER(zs_peer_out), i64, i64, i64,
+                                   vp, ctypes.c_size_t, vp]
+        L.zs_peer_wait.argtypes = [vp, i32, ctypes.c_uint32, vp]
+        L.zs_ipc_get_handle.argtypes = [vp, vp, ctypes.POINTER(i64)]
+        L.zs_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
+        L.zs_ipc_close.argtypes = [vp]
         for f in ("zs_encode_bound", "zs_encode_measure", "zs_encode", "zs_decompress", "zs_gemm",
-                  "zs_encode_measure_device", "zs_encode_device"):
+                  "zs_encode_measure_device", "zs_encode_device", "zs_gemm_peer", "zs_peer_wait",
+                  "zs_ipc_get_handle", "zs_ipc_open", "zs_ipc_close"):
             getattr(L, f).restype = ctypes.c_int
         L.zs_last_launch_count.restype = ctypes.c_int
         _lib = L
@@ -304,6 +328,72 @@ def gemm(x, w: ZsDevice, out=None, ws=None, stream=None):
                                     ctypes.c_void_p(out.data_ptr()), out.stride(0), M, N, K,
                                     ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream, x.device)))
     return out
+
+
+def peer_workspace(M: int, N: int, K: int, device):
+    """zs_gemm_peer workspace (zeroed once, self-cleaning counter + zs_gemm's workspace), kept
+    per device and path like workspace()."""
+    import torch
+    need = int(lib().zs_gemm_peer_workspace_bytes(M, N, K))
+    key = (str(device), int(lib().zs_gemm_is_decoupled(M, N, K)), "peer")
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws
+
+
+def gemm_peer(x, w: ZsDevice, ys, flags, rank: int, col0: int, epoch: int, ldy: int | None = None, ws=None,
+              stream=None):
+    """Column-sharded ZipGEMM with the output exchange fused into the kernel (zs_gemm_peer):
+    stores X @ W_shard^T into columns [col0, col0 + w.rows) of EVERY rank's Y and signals each
+    rank's flags[rank] = epoch.  ys / flags: per rank, a torch tensor on this device or an int
+    device address valid in this process (IPC-mapped peer memory)."""
+    import torch
+    assert x.dtype == torch.bfloat16 and x.dim() == 2 and x.stride(1) == 1
+    world = len(ys)
+    assert len(flags) == world and world <= MAX_PEERS   # the rest is validated by zs_gemm_peer
+    M, K = x.shape
+    N = w.rows
+    if ldy is None:
+        ldy = ys[rank].stride(0)
+    o = zs_peer_out()
+    o.world, o.rank, o.ldy, o.col0, o.epoch = world, rank, ldy, col0, epoch & 0xFFFFFFFF
+    for r in range(world):
+        o.y[r] = ys[r] if isinstance(ys[r], int) else ys[r].data_ptr()
+        o.flags[r] = flags[r] if isinstance(flags[r], int) else flags[r].data_ptr()
+    if ws is None:
+        ws = peer_workspace(M, N, K, x.device)
+    t = w.c_struct()
+    _check("zs_gemm_peer", lib().zs_gemm_peer(ctypes.c_void_p(x.data_ptr()), x.stride(0), ctypes.byref(t),
+                                              ctypes.byref(o), M, N, K, ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                              _stream_ptr(stream, x.device)))
+
+
+def peer_wait(flags, world: int, epoch: int, stream=None):
+    """Block the stream until this rank's flags[0..world) reached epoch (zs_peer_wait)."""
+    _check("zs_peer_wait", lib().zs_peer_wait(ctypes.c_void_p(flags.data_ptr()), world, epoch & 0xFFFFFFFF,
+                                              _stream_ptr(stream, flags.device)))
+
+
+def ipc_handle(t) -> tuple[bytes, int]:
+    """(handle bytes, byte offset) of the CUDA allocation holding torch tensor t."""
+    h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    off = ctypes.c_int64()
+    _check("zs_ipc_get_handle", lib().zs_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off)))
+    return h.raw, off.value
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map a peer's allocation (another process); returns its base address in this process."""
+    base = ctypes.c_void_p()
+    _check("zs_ipc_open", lib().zs_ipc_open(ctypes.create_string_buffer(handle, IPC_HANDLE_BYTES),
+                                            ctypes.byref(base)))
+    return base.value
+
+
+def ipc_close(base: int):
+    _check("zs_ipc_close", lib().zs_ipc_close(ctypes.c_void_p(base)))
 
 
 def last_launch_count() -> int:
