@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the cuBLAS / per-M context timings")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="N>1 output exchange: NCCL all-gather + permute, or the fused zs_gemm_peer epilogue "
+                         "(stores into every rank's Y over NVLink, CUDA IPC) + zs_peer_wait")
     return ap.parse_args()
 
 
@@ -229,16 +232,37 @@ def main():
     ws = Z.workspace(M, nloc, K, dev)
     stream = torch.cuda.current_stream(dev)
 
+    peer = None
+    if world > 1 and args.exchange == "peer":
+        # 3 output buffers: a rank's GEMM of step i+2 (whose signal lets the peers start
+        # step i+3, i.e. overwrite buffer i % 3) is ordered after its own reads of step i
+        peer = D.PeerOutputs(M, N, rank, world, dev, nbuf=3)
+        pws = Z.peer_workspace(M, nloc, K, dev)
+    epoch = [0]
+
+    def exchange_step(i, xin):
+        epoch[0] += 1
+        b = epoch[0] % 3
+        Z.gemm_peer(xin, wdev[i % R], peer.y_tables[b], peer.flag_table, rank, r0, epoch[0], ldy=N, ws=pws)
+        n = Z.last_launch_count()
+        Z.peer_wait(peer.flags, world, epoch[0])
+        return peer.y[b], n + 1
+
     def step(i, out_full=None):
+        if peer is not None:
+            return exchange_step(i, x)[0]
         Z.gemm(x, wdev[i % R], out=y, ws=ws)
         if world > 1:
             return D.gather_columns(y, world)
         return y
 
     # correctness gate on this very launch configuration (sampled, exact-size)
-    step(0)
+    if peer is not None:
+        _, launches_per_step = exchange_step(0, x)
+    else:
+        step(0)
+        launches_per_step = Z.last_launch_count()
     torch.cuda.synchronize()
-    launches_per_step = Z.last_launch_count()
 
     # CUDA graphs of S consecutive steps each (rotating through the weight copies): launch
     # overhead off the critical path, and consecutive ZipGEMMs in one graph overlap their
@@ -333,17 +357,28 @@ def main():
     for e in ev_yfree:
         e.record(stream)
 
+    ev_y3 = [torch.cuda.Event() for _ in range(3)]        # exchange: D2H of buffer b done
+    for e in ev_y3:
+        e.record(stream)
+
     def e2e_step(i):
         bsel = i & 1
         xd[bsel].copy_(xh, non_blocking=True)             # 256 KB at M = 32: same stream
         stream.wait_event(ev_yfree[bsel])
-        Z.gemm(xd[bsel], wdev[i % R], out=yd[bsel], ws=ws)
-        yy = D.gather_columns(yd[bsel], world) if world > 1 else yd[bsel]
+        if peer is not None:
+            # this step's signal lets the peers overwrite buffer (epoch + 1) % 3, which the
+            # D2H of two steps ago reads: wait for that copy first
+            stream.wait_event(ev_y3[(epoch[0] + 2) % 3])
+            yy = exchange_step(i, xd[bsel])[0]
+        else:
+            Z.gemm(xd[bsel], wdev[i % R], out=yd[bsel], ws=ws)
+            yy = D.gather_columns(yd[bsel], world) if world > 1 else yd[bsel]
         ev_y[bsel].record(stream)
         with torch.cuda.stream(cstream):
             cstream.wait_event(ev_y[bsel])
             yh[bsel].copy_(yy, non_blocking=True)
             ev_yfree[bsel].record(cstream)
+            ev_y3[epoch[0] % 3].record(cstream)          # D2H of buffer epoch % 3 done
 
     for i in range(min(args.warmup, 20)):
         e2e_step(i)
@@ -382,6 +417,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{layer} ZipGEMM M={M} (K={K}, N={N})", "layer": layer, "M": M, "K": K,
                        "N": N, "weights": "N(0,0.02^2) fp32 -> bf16 RNE, TCA-TBE", "parallelism": f"cols{world}",
+                       "exchange": (args.exchange if world > 1 else None),
                        "l2_hygiene": f"{R} rotated weight copies ({R * wbytes / 1e6:.0f} MB > 3x L2 {l2 / 1e6:.0f} MB)",
                        "bits_per_element": zh_full.bits_per_element(), "base_exp": zh_full.base_exp,
                        "coverage": zh_full.covered / (N * K), "graphs": graphs is not None,
