@@ -9,12 +9,10 @@
 //      and L segments) into the other stage: one load in flight per warp while it decodes.
 //   2. scan: lane l owns FragTiles 2l, 2l+1; popcounts of M = B1|B2|B3, a warp
 //      prefix scan over the 64 FragTiles, and per-row byte prefixes -> the H start of every
-//      FragTile row, stored as u16 in a table [o][r8] (two 16-B stores per lane).
-//   3. 16 passes, one TensorCoreTile (4 consecutive FragTiles in canonical order) each:
-//      lane -> (FragTile o = 4 pass + lane/8, row r8 = lane%8).  The 32 rows of a pass
-//      have CONTIGUOUS H bytes (~224 B), so the data-dependent H loads of the warp fall on
-//      distinct or broadcast banks instead of 32 random ones; the row decoder of
-//      zs_device.cuh; one 16-B store per lane (2 lanes = one full 32-B sector per row).
+//      FragTile row, stored as u16 in a bank-spread table [r8][o].
+//   3. 16 passes of 32 rows: lane -> (row lr = 4 pass + lane/8, FragTile column lane%8),
+//      the branch-free row decoder of zs_device.cuh, and one 16-B store per lane (8 lanes =
+//      one 128-B row segment, fully coalesced).
 #include "zs_device.cuh"
 #include "zs_kernels.h"
 #include "zs_lut.h"
@@ -22,7 +20,8 @@
 namespace zs {
 
 constexpr int kDecompMaxWarps = 16;
-constexpr uint32_t kHsTabBytes = 64 * 8 * 2;     // H-start table [o][r8] u16: 1 KB per warp
+constexpr uint32_t kHsRow = 80;                  // u16 per r8 row of the H-start table
+constexpr uint32_t kHsTabBytes = 8 * kHsRow * 2;  // 1280 B per warp
 
 __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(DecompParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -63,6 +62,11 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
   if (lane == 0 && bt < nbt) issue(bt, 0);
   __syncwarp();
 
+  // per-lane constants of the row passes
+  const int fc = lane & 7;                                  // FragTile column (K / 8)
+  const uint32_t ofc = (uint32_t)((fc >> 1) * 4 + (fc & 1) * 2);
+  const uint32_t smem_base = smem_u32(smem);
+  (void)smem_base;
   const uint32_t eb7x2 = p.eb7x2;
 
   for (uint32_t it = 0; bt < nbt; bt += G, ++it) {
@@ -90,7 +94,7 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
         if (lane >= d) incl += v;
       }
       const uint32_t s0 = incl - c0 - c1, s1 = s0 + c0;
-      // row prefix bytes of one FragTile -> H start of each of its 8 rows in [o][r8]
+      // row prefix bytes of one FragTile -> H start of each of its 8 rows in [r8][o]
       auto put = [&](uint32_t ml, uint32_t mh, uint32_t start, uint32_t o) {
         uint32_t bl = ml - ((ml >> 1) & 0x55555555u);
         bl = (bl & 0x33333333u) + ((bl >> 2) & 0x33333333u);
@@ -100,11 +104,11 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
         bh = (bh + (bh >> 4)) & 0x0F0F0F0Fu;
         const uint32_t pl = bl * 0x01010100u;                                   // rows 0..3
         const uint32_t ph = bh * 0x01010100u + ((bl * 0x01010101u) >> 24) * 0x01010101u;  // rows 4..7
-        // u16 pairs (rows 0,1 | 2,3 | 4,5 | 6,7): widen two prefix bytes, add start to both
-        const uint32_t s2 = start * 0x10001u;
-        *reinterpret_cast<uint4*>(hst + o * 8u) =
-            make_uint4(__byte_perm(pl, 0u, 0x4140u) + s2, __byte_perm(pl, 0u, 0x4342u) + s2,
-                       __byte_perm(ph, 0u, 0x4140u) + s2, __byte_perm(ph, 0u, 0x4342u) + s2);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          hst[r * kHsRow + o] = (uint16_t)(start + ((pl >> (8 * r)) & 0xFFu));
+          hst[(r + 4) * kHsRow + o] = (uint16_t)(start + ((ph >> (8 * r)) & 0xFFu));
+        }
       };
       put(m0l, m0h, s0, 2u * lane);
       put(m1l, m1h, s1, 2u * lane + 1u);
@@ -113,24 +117,24 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
 
     // ---- rows
     const int64_t br = bt / p.nbc, bc = bt - br * p.nbc;
-    const int g = lane >> 3, r8 = lane & 7;
-    const int64_t row0 = br * 64 + (g & 1) * 8 + r8;          // + 16 * (pass >> 2)
-    const int64_t col0 = bc * 64 + (g >> 1) * 8;              // + 16 * (pass & 3)
+    const int64_t col = bc * 64 + fc * 8;
+    const bool full_cols = p.vec_ok && (col + 8 <= p.cols);
 #pragma unroll 4
     for (int pass = 0; pass < 16; ++pass) {
-      const uint32_t o = 4u * pass + (uint32_t)g;              // canonical FragTile
+      const int lr = 4 * pass + (lane >> 3);                 // row inside the BlockTile
+      const int fr = lr >> 3, r8 = lr & 7;
+      const uint32_t o = (uint32_t)((fr >> 1) * 16 + (fr & 1)) + ofc;   // canonical FragTile
       const uint32_t b1 = st[o * 8 + r8];
       const uint32_t b2 = st[512 + o * 8 + r8];
       const uint32_t b3 = st[1024 + o * 8 + r8];
       const uint32_t m = b1 | b2 | b3;
-      const uint32_t hs = hst[o * 8 + r8];
+      const uint32_t hs = hst[r8 * kHsRow + o];
       const uint32_t ls = (o * 8 + (uint32_t)r8) * 8u - hs;
       const uint4 v = decode_row_core(b1, b2, b3, m, lut[m], H, hs, L, ls, eb7x2);
-      const int64_t row = row0 + 16 * (pass >> 2);
-      const int64_t col = col0 + 16 * (pass & 3);
+      const int64_t row = br * 64 + lr;
       if (row < p.rows) {
         uint16_t* dst = p.out + row * p.ld_out + col;
-        if (p.vec_ok && col + 8 <= p.cols) {
+        if (full_cols) {
           *reinterpret_cast<uint4*>(dst) = v;
         } else {
           const uint32_t w[4] = {v.x, v.y, v.z, v.w};
