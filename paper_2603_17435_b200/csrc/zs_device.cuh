@@ -415,6 +415,26 @@ __device__ __forceinline__ void spread_plane(uint32_t b, uint32_t& lo, uint32_t&
 //   Lrow: the row's first fallback value
 // Rows with >= 3 fallbacks (rank >= 2) are flagged by bit 7 of ent.x (the sign-replicate
 // bit of a selector nibble whose two modes give the same result) and patched on a rare path.
+// Fallback words of rank >= 2 in a row (the fast path merges ranks 0 and 1): one iteration
+// per such position -- the positions are the zero bits of m after its two lowest ones.
+__device__ __forceinline__ void patch_rank2(uint32_t m, const uint16_t* __restrict__ Lrow, uint32_t& o0,
+                                            uint32_t& o1, uint32_t& o2, uint32_t& o3) {
+  uint32_t z = ~m & 0xFFu;
+  z &= z - 1u;
+  z &= z - 1u;
+  while (z) {
+    const uint32_t i = __ffs(z) - 1u;
+    z &= z - 1u;
+    const uint32_t v = Lrow[i - __popc(m & ((1u << i) - 1u))];
+    const uint32_t sh = 16u * (i & 1u), keep = 0xFFFF0000u >> sh, ins = v << sh, j = i >> 1;
+    // named words, not an indexed array (an indexed array is demoted to local memory)
+    o0 = j == 0u ? ((o0 & keep) | ins) : o0;
+    o1 = j == 1u ? ((o1 & keep) | ins) : o1;
+    o2 = j == 2u ? ((o2 & keep) | ins) : o2;
+    o3 = j == 3u ? ((o3 & keep) | ins) : o3;
+  }
+}
+
 __device__ __forceinline__ uint4 decode_row_abs(uint32_t b1, uint32_t b2, uint32_t b3, uint32_t m, uint4 ent,
                                                 const uint32_t* __restrict__ H32, uint32_t hsh8,
                                                 const uint16_t* __restrict__ Lrow, uint32_t eb7x2) {
@@ -441,17 +461,7 @@ __device__ __forceinline__ uint4 decode_row_abs(uint32_t b1, uint32_t b2, uint32
     const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);            // + exponent field
     out[j] = prmt(lpair, w, mad_hi(sel[j], ZS_MUL(kM16, 1u << 16), 0u));      // fallback ranks 0/1
   }
-  if (ent.x & 0x80u) {  // rank >= 2 fallbacks: rare patch loop
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t rank = (uint32_t)i - __popc(m & ((1u << i) - 1u));
-      if (!((m >> i) & 1u) && rank >= 2) {
-        const uint32_t v = Lrow[rank];
-        const int j = i >> 1;
-        out[j] = (i & 1) ? ((out[j] & 0x0000FFFFu) | (v << 16)) : ((out[j] & 0xFFFF0000u) | v);
-      }
-    }
-  }
+  if (ent.x & 0x80u) patch_rank2(m, Lrow, out[0], out[1], out[2], out[3]);   // >= 3 fallbacks in the row: rare
   return make_uint4(out[0], out[1], out[2], out[3]);
 }
 
@@ -483,17 +493,7 @@ __device__ __forceinline__ uint4 decode_row_abs2(uint32_t b1, uint32_t b2, uint3
     const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);
     out[j] = prmt(lpair, w, fs[j]);
   }
-  if (ent.x & 0x80u) {  // rank >= 2 fallbacks: rare patch loop
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t rank = (uint32_t)i - __popc(m & ((1u << i) - 1u));
-      if (!((m >> i) & 1u) && rank >= 2) {
-        const uint32_t v = Lrow[rank];
-        const int j = i >> 1;
-        out[j] = (i & 1) ? ((out[j] & 0x0000FFFFu) | (v << 16)) : ((out[j] & 0xFFFF0000u) | v);
-      }
-    }
-  }
+  if (ent.x & 0x80u) patch_rank2(m, Lrow, out[0], out[1], out[2], out[3]);   // >= 3 fallbacks in the row: rare
   return make_uint4(out[0], out[1], out[2], out[3]);
 }
 

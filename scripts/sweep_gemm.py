@@ -23,6 +23,8 @@ ap.add_argument("--modes", default="auto", help="comma list of auto,fused,decoup
 ap.add_argument("--flags", default="0", help="comma list of zs_debug_set_flags values (timing experiments)")
 ap.add_argument("--graph-steps", type=int, default=1, help="GEMMs per captured graph (PDL needs >1)")
 ap.add_argument("--pdl", default="1", help="comma list of 0/1: programmatic dependent launch")
+ap.add_argument("--dist", default="gaussian", choices=["gaussian", "realistic"],
+                help="weights: N(0, 0.02^2), or per-row sigma 0.02*2^U(-1,1) + 0.1%% outliers at 20 sigma")
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -64,7 +66,8 @@ def timeit(fn, n_rot):
 
 for layer in a.layers.split(","):
     K, N = G.LAYERS[layer]
-    w = G.gaussian_bf16(N, K, 0.02, G.seed_of(layer))
+    w = (G.gaussian_bf16(N, K, 0.02, G.seed_of(layer)) if a.dist == "gaussian"
+         else G.realistic_bf16(N, K, seed=G.seed_of(layer)))
     zh = Z.encode(w)
     R = max(2, math.ceil(3 * l2 / zh.nbytes()))
     comp = [zh.to(dev) for _ in range(R)]
@@ -87,7 +90,7 @@ for layer in a.layers.split(","):
             if ring:
                 L.zs_debug_set_ring(ring)
             us = timeit(lambda i: Z.gemm(x, comp[i % R], out=y, ws=ws), R)
-            rec = {"layer": layer, "M": M, "mode": mode, "ring": ring, "flags": fl, "pdl": pdl,
+            rec = {"layer": layer, "dist": a.dist, "M": M, "mode": mode, "ring": ring, "flags": fl, "pdl": pdl,
                    "graph_steps": a.graph_steps, "us": round(us, 2),
                    "bits_per_el": round(zh.bits_per_element(), 3), "coverage": round(zh.covered / w.size, 4),
                    "tflops": round(2 * M * N * K / us / 1e6, 1),
