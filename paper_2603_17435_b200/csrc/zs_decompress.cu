@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
       if (row < p.rows) {
         uint16_t* dst = p.out + row * p.ld_out + col;
         if (full_cols) {
-          *reinterpret_cast<uint4*>(dst) = v;
+          __stcs(reinterpret_cast<uint4*>(dst), v);   // streaming store: the output is not re-read here
         } else {
           const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
