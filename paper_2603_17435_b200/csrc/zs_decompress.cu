@@ -20,6 +20,10 @@
 namespace zs {
 
 constexpr int kDecompMaxWarps = 16;
+#ifndef ZS_DECOMP_UNROLL
+#define ZS_DECOMP_UNROLL 4
+#endif
+constexpr int kDecompUnroll = ZS_DECOMP_UNROLL;   // row passes in flight per warp
 constexpr uint32_t kHsRow = 80;                  // u16 per r8 row of the H-start table
 constexpr uint32_t kHsTabBytes = 8 * kHsRow * 2;  // 1280 B per warp
 
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
     const int64_t br = bt / p.nbc, bc = bt - br * p.nbc;
     const int64_t col = bc * 64 + fc * 8;
     const bool full_cols = p.vec_ok && (col + 8 <= p.cols);
-#pragma unroll 4
+#pragma unroll kDecompUnroll
     for (int pass = 0; pass < 16; ++pass) {
       const int lr = 4 * pass + (lane >> 3);                 // row inside the BlockTile
       const int fr = lr >> 3, r8 = lr & 7;

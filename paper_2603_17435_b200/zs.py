@@ -85,10 +85,6 @@ def lib():
         L.zs_encode_device.argtypes = [vp, i64, i64, i64, i32, ctypes.POINTER(zs_sizes), vp, vp, vp, vp, vp, vp,
                                        ctypes.POINTER(zs_sizes), ctypes.POINTER(ctypes.c_uint16), vp, ctypes.c_size_t,
                                        vp]
-        if not hasattr(L, "zs_gemm_peer"):   # an older debug build (ZS_LIB): no exchange entry points
-            L.zs_last_launch_count.restype = ctypes.c_int
-            _lib = L
-            return L
         L.zs_gemm_peer_workspace_bytes.argtypes = [i64, i64, i64]
         L.zs_gemm_peer_workspace_bytes.restype = ctypes.c_size_t
         L.zs_gemm_peer.argtypes = [vp, i64, ctypes.POINTER(zs_tensor), ctypes.POINTER(zs_peer_out), i64, i64, i64,
