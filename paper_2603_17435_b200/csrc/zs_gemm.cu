@@ -66,7 +66,7 @@ constexpr uint32_t kRpTabBytes = 4 * kDecPerQuarter * kRpWarp;
 // stage header (u32 words): [4i+0..3] unit i {H a, H b, L a, L b} offsets inside the
 // stage regions; [20+i] unit i has BlockTile row b; [24] stage index the slot holds.
 
-struct __align__(8) Bars {
+struct __align__(16) Bars {
   uint64_t full_c[kMaxCSlots];
   uint64_t empty_c[kMaxCSlots];
   uint64_t xfull[kMaxXSlots / kUPS];     // per X-ring stage (4 tiles)
@@ -80,8 +80,6 @@ struct __align__(8) Bars {
   alignas(16) uint32_t dcount[kMaxASlots];  // lane quarters decoded into A slot a (monotonic, +4 per use)
 };
 
-// debug trace: trace[(cta * kTraceUnits + unit) * 16 + event] = clock64, first kTraceCtas CTAs
-constexpr int kTraceCtas = 4, kTraceUnits = 128;
 #ifndef ZS_REGSPLIT
 #define ZS_REGSPLIT 0   // setmaxnreg 72/40 split: measured 2x slower (spills in the 40-register roles)
 #endif
@@ -90,6 +88,8 @@ constexpr int kTraceCtas = 4, kTraceUnits = 128;
 #endif
 __device__ __forceinline__ void trace_ev(unsigned long long* tr, int unit, int ev) {
 #if ZS_TRACE
+  // debug trace: trace[(cta * kTraceUnits + unit) * 16 + event] = clock64, first kTraceCtas CTAs
+  constexpr int kTraceCtas = 4, kTraceUnits = 128;
   if (ZS_TRACE == 2 && ev >= 7 && ev < 16 && ev != 6 && (ev < 16) && (threadIdx.x >> 5) < kWarpEpi0) return;
   if (tr != nullptr && blockIdx.x < kTraceCtas && unit < kTraceUnits)
     tr[((size_t)blockIdx.x * kTraceUnits + unit) * 16 + ev] = clock64();

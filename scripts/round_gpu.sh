@@ -11,6 +11,7 @@ timeout 900 python scripts/sweep_gemm.py --layers L8B.GateUp,L8B.QKV,L8B.O,L8B.D
 timeout 900 python scripts/sweep_gemm.py --layers L8B.GateUp,L8B.QKV,L8B.O,L8B.Down --ms 256,512,2048,8192 --modes fused,decoupled --cublas --iters 20 > gpurun_out/sweep_large_${TAG}.jsonl 2>&1
 bash scripts/ncu_profile.sh ${TAG} 32 > gpurun_out/ncu_script_${TAG}.log 2>&1
 
+timeout 600 python scripts/sweep_gemm.py --layers L8B.GateUp,L8B.QKV,L8B.O,L8B.Down --ms 1,32 --dist realistic --cublas --graph-steps 10 > gpurun_out/sweep_realistic_${TAG}.jsonl 2>&1
 timeout 600 python scripts/peer_bench.py > gpurun_out/peer_${TAG}.jsonl 2>&1
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG}.log 2>&1
 ls -la gpurun_out
