@@ -128,7 +128,7 @@ zs_status zs_decompress(const zs_tensor *w, uint16_t *out, int64_t ld_out, void 
  * of at most ZS_GEMM_SMALL_NK elements switch at ZS_GEMM_LARGE_M_SMALL_NK tokens. */
 #define ZS_GEMM_LARGE_M 128
 #define ZS_GEMM_SMALL_NK (32ll * 1024 * 1024)
-#define ZS_GEMM_LARGE_M_SMALL_NK 32
+#define ZS_GEMM_LARGE_M_SMALL_NK 48
 
 /* Workspace (device bytes) zs_gemm needs for an M x N x K problem.
  *   fused path (zs_gemm_is_decoupled == 0): fp32 split-K partial sums [M][N] plus per-band arrival
