@@ -1,5 +1,6 @@
 // zs_kernels.h -- host-side launch interface of the sm_100a kernels (internal to libzs.so).
 #pragma once
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cuda.h>
@@ -29,6 +30,19 @@ size_t decompress_smem_bytes(uint32_t stage_bytes, int warps);
 int decompress_max_warps();
 
 constexpr int kMaxPeers = 8;   // ZS_MAX_PEERS
+
+// Run a kernel-attribute setter once per device (the attribute lives in the current
+// device's context).  Concurrent first calls may both run f, which is idempotent.
+template <typename F>
+inline cudaError_t once_per_device(std::atomic<uint64_t>& done, F&& f) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = f();
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 struct GemmParams {
   const uint64_t* b1;
