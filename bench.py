@@ -205,10 +205,18 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    # ZS_BENCH_ONE_GPU=1: every rank on cuda:0 over gloo -- a plumbing check of the N > 1
+    # paths on a one-GPU box (the ranks time-slice one GPU; the numbers mean nothing)
+    one_gpu = os.environ.get("ZS_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
@@ -318,7 +326,7 @@ def main():
     ms = t0.elapsed_time(t1)
     kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev) / S   # per launch (one ZipGEMM per step)
     if world > 1:
-        tt = torch.tensor([ms], device=dev)
+        tt = torch.tensor([ms], device="cpu" if one_gpu else dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     sec = ms / 1e3
@@ -419,7 +427,7 @@ def main():
     barrier()
     e2e_ms = e0.elapsed_time(e1)
     if world > 1:
-        tt = torch.tensor([e2e_ms], device=dev)
+        tt = torch.tensor([e2e_ms], device="cpu" if one_gpu else dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
     e2e_val = flops_step * args.steps / (e2e_ms / 1e3) / 1e12
