@@ -19,11 +19,18 @@
 
 namespace zs {
 
-constexpr int kDecompMaxWarps = 16;
+#ifndef ZS_DECOMP_WARPS
+#define ZS_DECOMP_WARPS 16
+#endif
+constexpr int kDecompMaxWarps = ZS_DECOMP_WARPS;   // independent decoder warps per CTA (one CTA per SM)
 #ifndef ZS_DECOMP_UNROLL
 #define ZS_DECOMP_UNROLL 4
 #endif
 constexpr int kDecompUnroll = ZS_DECOMP_UNROLL;   // row passes in flight per warp
+#ifndef ZS_DECOMP_STAGES
+#define ZS_DECOMP_STAGES 2
+#endif
+constexpr int kDecompStages = ZS_DECOMP_STAGES;   // smem stages per warp (BlockTiles in flight)
 constexpr uint32_t kHsRow = 80;                  // u16 per r8 row of the H-start table
 constexpr uint32_t kHsTabBytes = 8 * kHsRow * 2;  // 1280 B per warp
 
@@ -32,16 +39,16 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
   uint4* lut = reinterpret_cast<uint4*>(smem);   // 4 KB selector table
   const int nw = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 4096) + 2 * warp;
-  uint16_t* hst = reinterpret_cast<uint16_t*>(smem + 4096 + 16 * kDecompMaxWarps + warp * kHsTabBytes);
-  uint8_t* stage0 = smem + 4096 + 16 * kDecompMaxWarps + kDecompMaxWarps * kHsTabBytes +
-                    (size_t)warp * 2 * p.stage_bytes;
+  constexpr uint32_t kBarBytes = 8 * kDecompStages * kDecompMaxWarps;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 4096) + kDecompStages * warp;
+  uint16_t* hst = reinterpret_cast<uint16_t*>(smem + 4096 + kBarBytes + warp * kHsTabBytes);
+  uint8_t* stage0 = smem + 4096 + kBarBytes + kDecompMaxWarps * kHsTabBytes +
+                    (size_t)warp * kDecompStages * p.stage_bytes;
   const uint32_t stage_bytes = p.stage_bytes;
 
   for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = c_lut[i];
   if (lane == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int i = 0; i < kDecompStages; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   __syncthreads();   // lut visible (the only CTA-wide barrier)
@@ -63,21 +70,22 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
   };
 
   int64_t bt = (int64_t)blockIdx.x * nw + warp;
-  if (lane == 0 && bt < nbt) issue(bt, 0);
+  if (lane == 0)
+    for (int i = 0; i < kDecompStages - 1; ++i)
+      if (bt + i * G < nbt) issue(bt + i * G, i);
   __syncwarp();
 
   // per-lane constants of the row passes
   const int fc = lane & 7;                                  // FragTile column (K / 8)
   const uint32_t ofc = (uint32_t)((fc >> 1) * 4 + (fc & 1) * 2);
-  const uint32_t smem_base = smem_u32(smem);
-  (void)smem_base;
   const uint32_t eb7x2 = p.eb7x2;
 
   for (uint32_t it = 0; bt < nbt; bt += G, ++it) {
-    const int s = it & 1;
-    const int64_t nxt = bt + G;
-    if (lane == 0 && nxt < nbt) issue(nxt, s ^ 1);   // stage s^1 was consumed last iteration
-    mbar_wait(&bars[s], (it >> 1) & 1);
+    const int s = (int)(it % kDecompStages);
+    const int64_t nxt = bt + (kDecompStages - 1) * G;
+    // the stage consumed last iteration takes the BlockTile kDecompStages - 1 ahead
+    if (lane == 0 && nxt < nbt) issue(nxt, (int)((it + kDecompStages - 1) % kDecompStages));
+    mbar_wait(&bars[s], (it / kDecompStages) & 1);
 
     const uint8_t* st = stage0 + (size_t)s * stage_bytes;
     const uint8_t* H = st + 1536;
@@ -163,7 +171,8 @@ cudaError_t launch_decompress(const DecompParams& p, int grid, int warps, size_t
 }
 
 size_t decompress_smem_bytes(uint32_t stage_bytes, int warps) {
-  return 4096 + 16 * kDecompMaxWarps + kDecompMaxWarps * kHsTabBytes + (size_t)warps * 2 * stage_bytes;
+  return 4096 + 8 * kDecompStages * kDecompMaxWarps + kDecompMaxWarps * kHsTabBytes +
+         (size_t)warps * kDecompStages * stage_bytes;
 }
 
 int decompress_max_warps() { return kDecompMaxWarps; }
