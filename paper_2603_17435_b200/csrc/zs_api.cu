@@ -190,7 +190,7 @@ extern "C" zs_status zs_decompress(const zs_tensor* w, uint16_t* out, int64_t ld
 
 // split-K region: fp32 partials [min(M,256)][N] + per-band counters (zero between calls)
 static size_t splitk_bytes(int64_t M, int64_t N) {
-  const int64_t mc = std::min<int64_t>(M, 256);
+  const int64_t mc = up(std::min<int64_t>(M, 256), 16);   // row stride of the [N][mc] partials
   const int64_t nbands = (up(N, 64) / 64 + 1) / 2;
   return (size_t)up(mc * N * 4 + up(nbands * 4, 256), 256);
 }
@@ -280,7 +280,8 @@ static zs_status gemm_core(const uint16_t* x, int64_t ldx, const zs_tensor* w, u
   p.y = y;
   p.ldy = ldy;
   p.ws = reinterpret_cast<float*>(workspace);
-  p.counters = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(workspace) + mc_max * N * 4);
+  p.ldws = up(mc_max, 16);
+  p.counters = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(workspace) + p.ldws * N * 4);
   p.N = N;
   p.nbr = w->sz.padded_rows / 64;
   p.nbc = w->sz.padded_cols / 64;

@@ -165,6 +165,13 @@ __device__ __forceinline__ void signal_peers(uint32_t* done, uint32_t* const* fl
   if (f) st_release_sys(f, epoch);
 }
 
+// fire-and-forget fp32 vector reduction into global memory (16-B aligned)
+__device__ __forceinline__ void red_add_v4(float* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(__uint_as_float(a)),
+               "f"(__uint_as_float(b)), "f"(__uint_as_float(c)), "f"(__uint_as_float(d))
+               : "memory");
+}
+
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

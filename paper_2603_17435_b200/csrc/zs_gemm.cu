@@ -632,16 +632,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         uint32_t v[16];
         tmem_ld16(taddr + cb, v);
         if (nvalid) {
+          if (full) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int m = (int)cb + j;
-            if (m < p.mc) {
-              const float f = __uint_as_float(v[j]);
-              if (full)
-                p.y[(int64_t)(p.m0 + m) * p.ldy + n] = __bfloat16_as_ushort(__float2bfloat16_rn(f));
-              else
-                atomicAdd(p.ws + (int64_t)m * p.N + n, f);
+            for (int j = 0; j < 16; ++j) {
+              const int m = (int)cb + j;
+              if (m < p.mc)
+                p.y[(int64_t)(p.m0 + m) * p.ldy + n] = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(v[j])));
             }
+          } else {
+            // partial band: the thread's 16 token sums go to its workspace row [n][cb, cb+16)
+            // as four 16-B vector reductions (columns >= mc hold zeros: X is zero-filled)
+            float* wrow = p.ws + (int64_t)n * p.ldws + cb;
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) red_add_v4(wrow + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
           }
         }
       }
@@ -660,20 +663,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (bars->last_flag) {
           __threadfence();
           if (nvalid) {
-            // 16 independent loads in flight per batch (a rolled loop serialises one L2
-            // round trip per token: ~13 us at M = 32 on the kernel's critical tail)
-            for (int m0 = 0; m0 < p.mc; m0 += 16) {
-              float f[16];
+            // the thread's workspace row: 16-B loads, 4 in flight per batch of 16 tokens, then
+            // zeroed again with 16-B stores (self-cleaning)
+            float4* wrow = reinterpret_cast<float4*>(p.ws + (int64_t)n * p.ldws);
+            for (int m0 = 0; m0 < (int)p.n_umma; m0 += 16) {
+              float4 f[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) f[j] = __ldcg(wrow + m0 / 4 + j);
+              const float* g = reinterpret_cast<const float*>(f);
 #pragma unroll
               for (int j = 0; j < 16; ++j)
-                f[j] = (m0 + j < p.mc) ? __ldcg(p.ws + (int64_t)(m0 + j) * p.N + n) : 0.0f;
+                if (m0 + j < p.mc)
+                  p.y[(int64_t)(p.m0 + m0 + j) * p.ldy + n] = __bfloat16_as_ushort(__float2bfloat16_rn(g[j]));
 #pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                if (m0 + j < p.mc) {
-                  p.y[(int64_t)(p.m0 + m0 + j) * p.ldy + n] = __bfloat16_as_ushort(__float2bfloat16_rn(f[j]));
-                  __stcg(p.ws + (int64_t)(m0 + j) * p.N + n, 0.0f);
-                }
-              }
+              for (int j = 0; j < 4; ++j) __stcg(wrow + m0 / 4 + j, make_float4(0.f, 0.f, 0.f, 0.f));
             }
           }
           if (kPeer && nvalid && p.npeer > 0)

@@ -53,7 +53,8 @@ struct GemmParams {
   const uint64_t* offsets;
   uint16_t* y;
   int64_t ldy;
-  float* ws;                // [256][N] fp32 split-K partials (zero between calls)
+  float* ws;                // [N][ldws] fp32 split-K partials, row n = weight row (zero between calls)
+  int64_t ldws;             // workspace row stride (floats): roundup(min(M, 256), 16) >= n_umma
   uint32_t* counters;       // [nbands] arrival counters (zero between calls)
   int64_t N;                // logical output features
   int64_t nbr, nbc;         // BlockTile grid
