@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
                     (size_t)warp * kDecompStages * p.stage_bytes;
   const uint32_t stage_bytes = p.stage_bytes;
 
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = c_lut[i];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = __ldg(&c_lut[i]);
   if (lane == 0) {
     for (int i = 0; i < kDecompStages; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();

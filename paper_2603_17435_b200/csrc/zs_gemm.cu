@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   // ---- setup
   if (tid < 256) {
-    const uint4 e = c_lut[tid];
+    const uint4 e = __ldg(&c_lut[tid]);
     slut[2 * tid] = e;
     slut[2 * tid + 1] = make_uint4(e.x >> 16, e.y >> 16, e.z >> 16, e.w >> 16);
   }
