@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("ZS_LIB") or os.path.join(_PKG, "libzs.so")   # ZS_LIB
 ZS_STATUS = {0: "ZS_OK", 1: "ZS_ERR_INVALID_ARG", 2: "ZS_ERR_SHAPE", 3: "ZS_ERR_ALIGNMENT",
              4: "ZS_ERR_UNSUPPORTED", 5: "ZS_ERR_CORRUPT", 6: "ZS_ERR_CUDA", 7: "ZS_ERR_CAPACITY"}
 
-# every symbol include/zs.h declares (checked by tests/test_abi.py)
+# every symbol include/zs.h declares (checked by tests/test_abi_encode.py)
 EXPORTS = ["zs_encode_bound", "zs_encode_measure", "zs_encode", "zs_decompress", "zs_gemm_workspace_bytes",
            "zs_gemm_is_decoupled", "zs_gemm", "zs_last_launch_count", "zs_status_string",
            "zs_encode_device_workspace_bytes", "zs_encode_measure_device", "zs_encode_device",

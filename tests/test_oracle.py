@@ -269,7 +269,9 @@ def test_lane_equals_sequential_random_fragments():
     # SPEC acceptance #2, >= 1e4 random fragments: 160 BlockTiles x 64 FragTiles
     rng = np.random.default_rng(11)
     w = rng.integers(0, 65536, size=(640, 1024), dtype=np.uint64).astype(np.uint16)
-    w[rng.random(w.shape) < 0.7] = G.gaussian_bf16(640, 1024, 0.02, 2)[rng.random(w.shape) < 0.7][:1]
+    mask = rng.random(w.shape) < 0.7            # ~70% Gaussian (in-window), the rest raw patterns
+    g = G.gaussian_bf16(640, 1024, 0.02, 2)
+    w[mask] = g[mask]
     e = O.encode(w)
     assert e.n_fragtiles >= 10_000
     np.testing.assert_array_equal(O.decode_lanes(e), O.decode_sequential(e))
@@ -386,3 +388,24 @@ def test_gaussian_exponent_entropy_range():
     ps = np.array([O.gaussian_pmf(0.02, x) for x in range(-60, 11)])
     ps = ps[ps > 0]
     assert abs(h + float((ps * np.log2(ps)).sum())) < 0.05
+
+
+def test_coverage_ratio_topk_pins():
+    # r_n: fraction of elements covered by the 2^n - 1 most frequent exponents.
+    # Closed forms: uniform histogram -> (2^n - 1) / 256; one spike -> 1.
+    u = np.ones(256, np.int64)
+    for n in range(1, 9):
+        assert O.coverage_ratio_topk(u, n) == pytest.approx((2 ** n - 1) / 256, abs=1e-15)
+    spike = np.zeros(256, np.int64)
+    spike[120] = 99
+    assert O.coverage_ratio_topk(spike, 1) == 1.0
+    # Theorem 2 (contiguity): for a Gaussian the top 2^n - 1 exponents form one
+    # contiguous window, so r_3 equals the coverage of the max-coverage 7-window (Alg. 1)
+    w = G.gaussian_bf16(1024, 1024, 0.02, 7)
+    h = O.histogram(w)
+    _, cov = O.select_window(h)
+    assert O.coverage_ratio_topk(h, 3) == pytest.approx(cov / h.sum(), abs=1e-15)
+    # ... and r_3 of the sampled histogram agrees with the Appendix A pmf (bf16 rounding and
+    # sampling error only)
+    ps = np.sort(np.array([O.gaussian_pmf(0.02, x) for x in range(-60, 11)]))[::-1]
+    assert O.coverage_ratio_topk(h, 3) == pytest.approx(ps[:7].sum(), abs=3e-3)
