@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the cuBLAS / per-M context timings")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--plumbing-check", action="store_true",
+                    help="CPU-only check of the N-rank harness (spawn, gloo process group, max-over-ranks timing, "
+                         "rank-0 line) with a numpy stand-in step; prints a line marked as not a measurement")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
                     help="N>1 output exchange: NCCL all-gather + permute, or the fused zs_gemm_peer epilogue "
                          "(stores into every rank's Y over NVLink, CUDA IPC) + zs_peer_wait")
@@ -118,31 +121,75 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle legs
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
 def oracle_sample(layer, M, seconds_budget):
-    """Time the CPU oracle (decode + fp64 GEMM, as it stands) on a bounded row sample."""
+    """Time the CPU oracle (decode + fp64 GEMM, as it stands) on a bounded row sample: once on
+    one core, then with one worker thread per host core on disjoint row blocks (the oracle is
+    plain C called through ctypes, which releases the GIL, so the threads run in parallel)."""
+    import concurrent.futures as cf
+
     import oracle as O
     K, N = G.LAYERS[layer]
-    w_all = None
-    rows = 64
-    w = G.gaussian_bf16(N, K, 0.02, G.seed_of(layer))[:4096]  # same seeded weights, first rows
+    w = G.gaussian_bf16(N, K, 0.02, G.seed_of(layer))[:8192]   # same seeded weights, first rows
     x = G.activations_bf16(M, K, seed=G.seed_of(layer + ".X") + M)
-    del w_all
+    eb = O.encode(w[:64]).base_exp
+    encs = {}
 
-    def run(r):
-        enc = O.encode(w[:r], base_exp=O.encode(w[:64]).base_exp)  # offline, untimed
-        t0 = time.perf_counter()
-        wd = O.decode_sequential(enc)
+    def enc(r0, r1):                                            # offline, untimed
+        if (r0, r1) not in encs:
+            encs[(r0, r1)] = O.encode(w[r0:r1], base_exp=eb)
+        return encs[(r0, r1)]
+
+    def work(r0, r1):
+        wd = O.decode_sequential(enc(r0, r1))
         O.gemm_f64(x, wd)
+
+    def timed_single(rows):
+        enc(0, rows)
+        t0 = time.perf_counter()
+        work(0, rows)
         return time.perf_counter() - t0
 
-    t = run(rows)
+    rows = 64
+    t = timed_single(rows)
     if t < seconds_budget:
         rows = int(min(4096, max(64, (seconds_budget / t) * rows)) // 64 * 64)
-        t = run(rows)
-    flops = 2.0 * M * rows * K
-    return {"value": flops / t / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": "oracle",
-            "sample": f"{layer} rows [0,{rows}) of N={N}, K={K}, M={M}: oracle decode_sequential + fp64 gemm, "
-                      f"{t:.2f} s single-threaded"}
+        t = timed_single(rows)
+    single = 2.0 * M * rows * K / t / 1e12
+    # all cores: `cores` threads, each on its own 64-row-aligned block, sized like the single run
+    cores = host_cores()
+    per = max(64, min(8192 // cores // 64 * 64, rows)) if cores > 1 else rows
+    blocks = [(i * per, (i + 1) * per) for i in range(cores) if (i + 1) * per <= 8192]
+    for b in blocks:
+        enc(*b)
+    with cf.ThreadPoolExecutor(len(blocks)) as ex:
+        t0 = time.perf_counter()
+        list(ex.map(lambda b: work(*b), blocks))
+        tall = time.perf_counter() - t0
+    allv = 2.0 * M * per * len(blocks) * K / tall / 1e12
+    return {"value": allv, "unit": "TFLOP/s", "cores": len(blocks), "kind": "oracle",
+            "sample": f"{layer} rows [0,{per * len(blocks)}) of N={N}, K={K}, M={M}: oracle decode_sequential + "
+                      f"fp64 gemm, {len(blocks)} threads x {per} rows in {tall:.2f} s",
+            "single_core": {"value": single, "cores": 1,
+                            "sample": f"rows [0,{rows}) in {t:.2f} s on one thread"},
+            "cpu": cpu_model()}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:  # pragma: no cover
+        pass
+    return None
 
 
 def run_reference(args):
@@ -178,7 +225,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{layer} ZipGEMM M={M} (K={K}, N={N})", "layer": layer, "M": M, "K": K, "N": N},
-        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
                          "sample": f"per step: oracle decode of one 64x{K} BlockTile row band + fp64 gemm of {r} "
                                    f"rows at M={M}"},
         "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -190,10 +237,110 @@ def metric_name():
 
 
 # ------------------------------------------------------------------ GPU arm
+def spawn_ranks(args):
+    """`bench.py --gpus N` without a launcher: start N copies of this script as ranks
+    0..N-1 (one process per GPU, rendezvous on 127.0.0.1) and wait for them; rank 0 prints
+    the line.  Under torchrun (WORLD_SIZE set) this is skipped."""
+    import socket
+    import subprocess
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env))
+    rcs = [p.wait() for p in procs]
+    sys.exit(max(rcs))
+
+
+def init_ranks(args, need_gpu=True):
+    """(world, rank, local, device, backend) of this process; joins the process group."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    # ZS_BENCH_ONE_GPU=1: every rank on cuda:0 over gloo -- a plumbing check of the N > 1
+    # paths on a one-GPU box (the ranks time-slice one GPU; the numbers mean nothing)
+    one_gpu = os.environ.get("ZS_BENCH_ONE_GPU") == "1" or not need_gpu
+    if one_gpu:
+        local = 0
+    dev = None
+    if need_gpu:
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+    backend = None
+    if world > 1:
+        backend = "gloo" if one_gpu else "nccl"
+        if backend == "nccl":
+            # communicator init is logged (to stderr, so stdout keeps its one JSON line)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, local, dev, backend
+
+
+def reduce_max(v, world, dev):
+    """max over ranks of a host float (the contract's max-over-ranks timing)."""
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], device=dev if dev is not None and dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def plumbing_check(args):
+    """The N-rank harness on CPU (gloo): same spawn / process group / barrier / max-over-ranks
+    / rank-0 line as the GPU arm, with a numpy stand-in for the step.  Not a measurement."""
+    import torch
+    import torch.distributed as dist
+    world, rank, _, _, backend = init_ranks(args, need_gpu=False)
+    a = np.ones((64, 64)) * (rank + 1)
+    for _ in range(args.warmup):
+        a @ a
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        y = torch.from_numpy((a @ a)[:1].copy())
+        if world > 1:
+            buf = [torch.empty_like(y) for _ in range(world)]
+            dist.all_gather(buf, y)
+            y = torch.cat(buf, 1)
+    if world > 1:
+        dist.barrier()
+    ms = reduce_max((time.perf_counter() - t0) * 1e3, world, None)
+    ok = y.shape[1] == 64 * world and all(float(y[0, 64 * r]) == 64.0 * (r + 1) ** 2 for r in range(world))
+    if rank == 0:
+        print(json.dumps({"metric": metric_name(), "value": None, "unit": "TFLOP/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                          "data": "plumbing-check (CPU numpy stand-in, not a measurement)",
+                          "config": {"workload": "plumbing-check", "parallelism": f"cols{world}",
+                                     "backend": backend, "gathered_ok": bool(ok)}}))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
+        return
+    if args.plumbing_check:
+        plumbing_check(args)
         return
     import torch
     import torch.distributed as dist
@@ -201,22 +348,8 @@ def main():
     import paper_2603_17435_b200 as Z
     from paper_2603_17435_b200 import dist as D
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
-    # ZS_BENCH_ONE_GPU=1: every rank on cuda:0 over gloo -- a plumbing check of the N > 1
-    # paths on a one-GPU box (the ranks time-slice one GPU; the numbers mean nothing)
-    one_gpu = os.environ.get("ZS_BENCH_ONE_GPU") == "1"
-    if one_gpu:
-        local = 0
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        if one_gpu:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
+    world, rank, local, dev, backend = init_ranks(args)
+    one_gpu = backend == "gloo"
 
     def barrier():
         if world > 1:
@@ -264,13 +397,20 @@ def main():
             return D.gather_columns(y, world)
         return y
 
-    # correctness gate on this very launch configuration (sampled, exact-size)
+    # correctness gate on this very launch configuration: sampled output columns against a
+    # dense fp32 torch matmul of the uncompressed weight rows (north-star error metric C15)
     if peer is not None:
-        _, launches_per_step = exchange_step(0, x)
+        yg, launches_per_step = exchange_step(0, x)
     else:
-        step(0)
+        yg = step(0)
         launches_per_step = Z.last_launch_count()
     torch.cuda.synchronize()
+    cols = np.unique(np.linspace(0, N - 1, 97).astype(np.int64))
+    wc = torch.from_numpy(w[cols].view(np.int16)).view(torch.bfloat16).to(dev).float()
+    yref = x.float() @ wc.t()
+    scale = x.float().abs() @ wc.abs().t()
+    gate_err = float(((yg[:, torch.from_numpy(cols).to(dev)].float() - yref).abs() / scale.clamp_min(1e-30)).max())
+    assert gate_err <= 1e-2, f"bench correctness gate failed: err {gate_err}"
 
     # CUDA graphs of S consecutive steps each (rotating through the weight copies): launch
     # overhead off the critical path, and consecutive ZipGEMMs in one graph overlap their
@@ -325,10 +465,9 @@ def main():
         barrier()
     ms = t0.elapsed_time(t1)
     kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev) / S   # per launch (one ZipGEMM per step)
-    if world > 1:
-        tt = torch.tensor([ms], device="cpu" if one_gpu else dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = reduce_max(ms, world, dev)
+    multi = multi_gpu_breakdown(args, Z, D, x, y, ws, wdev, R, world, rank, dev, stream, zh_full, M, K, N, ms / args.steps,
+                                exchange=peer is not None) if world > 1 else None
     sec = ms / 1e3
     flops_step = 2.0 * M * N * K
     bytes_step_alg = zh_full.nbytes() + 2.0 * M * K * world + 2.0 * M * N
@@ -428,11 +567,7 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    e2e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        tt = torch.tensor([e2e_ms], device="cpu" if one_gpu else dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+    e2e_ms = reduce_max(e0.elapsed_time(e1), world, dev)
     e2e_val = flops_step * args.steps / (e2e_ms / 1e3) / 1e12
 
     extras = {}
@@ -466,11 +601,56 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
         }
+        line["config"]["gate_err"] = gate_err
+        if multi:
+            line["multi_gpu"] = multi
         if extras:
             line["context"] = extras
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def multi_gpu_breakdown(args, Z, D, x, y, ws, wdev, R, world, rank, dev, stream, zh_full, M, K, N, step_ms,
+                        exchange):
+    """Per-rank split of the N-GPU step (max over ranks of each part): the shard's ZipGEMM
+    alone, the NCCL all-gather + permute alone, the whole step, and T_1 / (w T_w) with T_1 the
+    unsharded ZipGEMM timed on this GPU (6.5)."""
+    import torch
+
+    def timed(fn, n):
+        for i in range(3):
+            fn(i)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(n):
+            fn(i)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+
+    n = max(10, min(args.steps, 200))
+    gemm_ms = timed(lambda i: Z.gemm(x, wdev[i % R], out=y, ws=ws), n)
+    gather_ms = timed(lambda i: D.gather_columns(y, world), n) if not exchange else None
+    out = {"gemm_us": reduce_max(gemm_ms, world, dev) * 1e3,
+           "allgather_us": (reduce_max(gather_ms, world, dev) * 1e3) if gather_ms is not None else None,
+           "step_us": step_ms * 1e3, "backend": "nccl" if not os.environ.get("ZS_BENCH_ONE_GPU") else "gloo"}
+    try:
+        out["nccl_version"] = ".".join(str(v) for v in torch.cuda.nccl.version())
+    except Exception:  # pragma: no cover
+        pass
+    if rank == 0:
+        l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+        nf = max(2, math.ceil(3 * l2 / zh_full.nbytes()))
+        full = [zh_full.to(dev) for _ in range(nf)]
+        yf = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+        wsf = Z.workspace(M, N, K, dev)
+        t1 = timed(lambda i: Z.gemm(x, full[i % nf], out=yf, ws=wsf), n)
+        out["t1_us"] = t1 * 1e3
+        out["t1_over_w_tw"] = t1 / (world * step_ms)
+        del full
+    return out
 
 
 def context_timings(Z, zh, w, layer, K, N, dev, R, l2):

@@ -18,8 +18,23 @@
  * This ABI uses the F.linear convention: X is [M tokens][K], W is [N out][K], Y is [M][N].
  *
  * Conventions for every call
- *   - Ownership: the caller owns every buffer.  The library never allocates device
- *     memory and keeps no global mutable state (thread-safe for concurrent callers).
+ *   - Ownership: the caller owns every buffer.  The library allocates no device memory
+ *     for data; the only library-held state is (a) one cuBLAS handle per (host thread,
+ *     device), created by the first zs_gemm call that takes the decoupled large-M path
+ *     (cublasCreate allocates a small device workspace -- make that first call outside
+ *     CUDA-graph capture), (b) a per-thread launch count (zs_last_launch_count) and a
+ *     per-thread X tensor-map cache, (c) the zs_debug_* experiment knobs of zs_api.cu,
+ *     which are NOT part of this ABI: process-global, not synchronised, for the repo's
+ *     own timing scripts only (they change kernel behaviour and, for
+ *     zs_debug_set_large_m, what zs_gemm_workspace_bytes returns).  With the knobs left
+ *     alone every entry point is thread-safe for concurrent callers.
+ *   - Launch mode: zs_gemm / zs_gemm_peer launch with programmatic dependent launch
+ *     (PDL).  Their compressed-weight producer reads W and its offsets BEFORE
+ *     griddepcontrol.wait, so the kernel launched immediately before them on the same
+ *     stream must not write the encoded W (X, Y and the workspace are read/written only
+ *     after the wait).  Encoded weights are immutable by contract, so this only matters
+ *     to a caller that re-encodes into the same buffers on the GEMM's stream: put an
+ *     event or any non-PDL launch between the two.
  *   - Device calls are asynchronous on `stream` (a cudaStream_t passed as void*;
  *     NULL = legacy default stream).  Validation is synchronous and happens before
  *     launch; no exceptions cross the ABI.  Launch failures return ZS_ERR_CUDA.

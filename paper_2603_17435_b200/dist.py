@@ -144,6 +144,9 @@ class ShardedZipLinear:
     def __call__(self, x):
         from .zs import gemm, gemm_peer, peer_wait
         if self.exchange == "peer":
+            # the exchanged buffers are [M][N] on every rank: a larger x would make every
+            # rank's epilogue store past the end of its peers' IPC-mapped outputs
+            assert x.shape[0] == self.peer.M, f"exchange='peer' was built for M={self.peer.M}, got {x.shape[0]}"
             self.step += 1
             b = self.step % len(self.peer.y)
             gemm_peer(x, self.dev, self.peer.y_tables[b], self.peer.flag_table, self.rank, self.r0, self.step,

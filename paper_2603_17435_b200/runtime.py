@@ -16,7 +16,7 @@ device buffers, streams, events and the graph capture -- no compute of its own.
 """
 from __future__ import annotations
 
-from .zs import ZsDevice, gemm, last_launch_count, workspace
+from .zs import ZsDevice, gemm, last_launch_count, lib
 
 
 class GraphedZipLinear:
@@ -30,7 +30,9 @@ class GraphedZipLinear:
         self.y_host = torch.zeros((steps, M, N), dtype=bf16).pin_memory()
         self._xd = [torch.zeros((M, K), dtype=bf16, device=dev) for _ in range(steps)]
         self._yd = [torch.zeros((M, N), dtype=bf16, device=dev) for _ in range(steps)]
-        self._ws = workspace(M, N, K, dev)
+        # a private, zero-initialised workspace: the graph captures its address, and another
+        # executor's graph (or an eager zs.gemm) may run concurrently on another stream
+        self._ws = torch.zeros(max(int(lib().zs_gemm_workspace_bytes(M, N, K)), 16), dtype=torch.uint8, device=dev)
         main, h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         ev_x = [torch.cuda.Event() for _ in range(steps)]
         ev_y = [torch.cuda.Event() for _ in range(steps)]

@@ -295,15 +295,27 @@ def decompress(w: ZsDevice, out=None, stream=None):
 _WS = {}
 
 
-def workspace(M: int, N: int, K: int, device):
-    """zs_gemm workspace, kept per device and grown on demand: the zero-initialised,
-    self-cleaning split-K buffer of the fused path, or the decoded-weight scratch of the
-    decoupled (large-M) path -- two separate buffers, since the latter is left dirty."""
+def _stream_key(stream, device):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return int(stream.cuda_stream)
+
+
+def workspace(M: int, N: int, K: int, device, stream=None):
+    """zs_gemm workspace, kept per (device, stream, path) and grown on demand: the
+    zero-initialised, self-cleaning split-K buffer of the fused path, or the decoded-weight
+    scratch of the decoupled (large-M) path -- separate buffers, since the latter is left dirty.
+    include/zs.h allows a workspace to be reused only in stream order, so each stream gets
+    its own; a buffer replaced by a larger one is released only after a synchronisation of
+    its stream (a kernel queued on it may still use it)."""
     import torch
     need = int(lib().zs_gemm_workspace_bytes(M, N, K))
-    key = (str(device), int(lib().zs_gemm_is_decoupled(M, N, K)))
+    key = (str(device), _stream_key(stream, device), int(lib().zs_gemm_is_decoupled(M, N, K)))
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
+        if ws is not None:
+            torch.cuda.synchronize(device)
         ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)
         _WS[key] = ws
     return ws
@@ -318,7 +330,7 @@ def gemm(x, w: ZsDevice, out=None, ws=None, stream=None):
     if out is None:
         out = torch.empty((M, N), dtype=torch.bfloat16, device=x.device)
     if ws is None:
-        ws = workspace(M, N, K, x.device)
+        ws = workspace(M, N, K, x.device, stream)
     t = w.c_struct()
     _check("zs_gemm", lib().zs_gemm(ctypes.c_void_p(x.data_ptr()), x.stride(0), ctypes.byref(t),
                                     ctypes.c_void_p(out.data_ptr()), out.stride(0), M, N, K,
@@ -326,14 +338,16 @@ def gemm(x, w: ZsDevice, out=None, ws=None, stream=None):
     return out
 
 
-def peer_workspace(M: int, N: int, K: int, device):
+def peer_workspace(M: int, N: int, K: int, device, stream=None):
     """zs_gemm_peer workspace (zeroed once, self-cleaning counter + zs_gemm's workspace), kept
-    per device and path like workspace()."""
+    per (device, stream, path) like workspace()."""
     import torch
     need = int(lib().zs_gemm_peer_workspace_bytes(M, N, K))
-    key = (str(device), int(lib().zs_gemm_is_decoupled(M, N, K)), "peer")
+    key = (str(device), _stream_key(stream, device), int(lib().zs_gemm_is_decoupled(M, N, K)), "peer")
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
+        if ws is not None:
+            torch.cuda.synchronize(device)
         ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)
         _WS[key] = ws
     return ws
@@ -353,13 +367,18 @@ def gemm_peer(x, w: ZsDevice, ys, flags, rank: int, col0: int, epoch: int, ldy: 
     N = w.rows
     if ldy is None:
         ldy = ys[rank].stride(0)
+    # Y buffers are [M][ldy]: the kernel stores M rows into every rank's buffer, so every
+    # buffer this process can see must have them (peer buffers are the same shape by contract)
+    for r in range(world):
+        if not isinstance(ys[r], int):
+            assert ys[r].shape[0] >= M and ys[r].stride(0) == ldy, f"ys[{r}] smaller than [M={M}][ldy={ldy}]"
     o = zs_peer_out()
     o.world, o.rank, o.ldy, o.col0, o.epoch = world, rank, ldy, col0, epoch & 0xFFFFFFFF
     for r in range(world):
         o.y[r] = ys[r] if isinstance(ys[r], int) else ys[r].data_ptr()
         o.flags[r] = flags[r] if isinstance(flags[r], int) else flags[r].data_ptr()
     if ws is None:
-        ws = peer_workspace(M, N, K, x.device)
+        ws = peer_workspace(M, N, K, x.device, stream)
     t = w.c_struct()
     _check("zs_gemm_peer", lib().zs_gemm_peer(ctypes.c_void_p(x.data_ptr()), x.stride(0), ctypes.byref(t),
                                               ctypes.byref(o), M, N, K, ctypes.c_void_p(ws.data_ptr()), ws.numel(),
