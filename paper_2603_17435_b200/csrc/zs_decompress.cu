@@ -78,7 +78,9 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
   // per-lane constants of the row passes
   const int fc = lane & 7;                                  // FragTile column (K / 8)
   const uint32_t ofc = (uint32_t)((fc >> 1) * 4 + (fc & 1) * 2);
-  const uint32_t eb7x2 = p.eb7x2;
+  DecConst dk;
+  load_dec_const(dk, p.eb7x2);
+  const uint32_t lut_b = smem_u32(lut);
 
   for (uint32_t it = 0; bt < nbt; bt += G, ++it) {
     const int s = (int)(it % kDecompStages);
@@ -88,8 +90,8 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
     mbar_wait(&bars[s], (it / kDecompStages) & 1);
 
     const uint8_t* st = stage0 + (size_t)s * stage_bytes;
-    const uint8_t* H = st + 1536;
-    const uint16_t* L = reinterpret_cast<const uint16_t*>(st + 1536 + p.hcap);
+    const uint32_t Hs = smem_u32(st + 1536);             // H segment (16-B aligned)
+    const uint32_t Ls = smem_u32(st + 1536 + p.hcap);    // L segment
 
     // ---- scan: FragTiles 2*lane, 2*lane+1 (canonical order)
     {
@@ -142,7 +144,9 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
       const uint32_t m = b1 | b2 | b3;
       const uint32_t hs = hst[r8 * kHsRow + o];
       const uint32_t ls = (o * 8 + (uint32_t)r8) * 8u - hs;
-      const uint4 v = decode_row_core(b1, b2, b3, m, lut[m], H, hs, L, ls, eb7x2);
+      uint4 v = decode_row_v3(b1, b2, b3, ld_shared_v4(lut_b + 16u * m), Hs + (hs & ~3u), hs * 8u, Ls + 2u * ls, dk);
+      if (lut[m].x & 0x80u)   // >= 3 fallbacks in the row (rank >= 2): rare patch
+        patch_rank2(m, reinterpret_cast<const uint16_t*>(st + 1536 + p.hcap) + ls, v.x, v.y, v.z, v.w);
       const int64_t row = br * 64 + lr;
       if (row < p.rows) {
         uint16_t* dst = p.out + row * p.ld_out + col;

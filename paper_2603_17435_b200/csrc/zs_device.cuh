@@ -77,11 +77,20 @@ static __device__ __noinline__ void zs_watchdog_fire(const void* what, uint32_t 
   __trap();
 }
 
+__device__ __forceinline__ uint64_t globaltimer_now() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Wait for the phase with the given parity.  After one plain probe the waiting warp is
+// suspended in hardware (try_wait with a time hint: it resumes when the phase completes),
+// so a waiting role costs no issue slots on the SMSP it shares with decoder warps.  The
+// watchdog is time based (checked every 256 suspended probes): > 10 s traps.
+static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity);
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t n = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if (++n == (1u << 28)) zs_watchdog_fire(bar, parity);
-  }
+  if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
 }
 
 // for idle roles (epilogue): try_wait with a suspend-time hint -- the warp is descheduled
@@ -98,15 +107,15 @@ __device__ __forceinline__ bool mbar_try_wait_suspend(uint64_t* bar, uint32_t pa
   return ok != 0;
 }
 
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  uint32_t n = 0;
-  while (!mbar_try_wait_suspend(bar, parity, 1000000u)) {
-    if (++n == (1u << 20)) zs_watchdog_fire(bar, parity);
+static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
+  uint64_t t0 = 0;
+  for (uint32_t n = 1; !mbar_try_wait_suspend(bar, parity, 0x100000u); ++n) {
+    if ((n & 255u) == 0u) {
+      const uint64_t t = globaltimer_now();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 10000000000ull) zs_watchdog_fire(bar, parity);
+    }
   }
-}
-
-__device__ __forceinline__ void st_release_shared(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ uint32_t ld_acquire_shared(const uint32_t* p) {
@@ -125,15 +134,6 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
-}
-
-// CTA-completion counter of the exchange: release orders this CTA's output stores (made
-// visible to this thread by the preceding CTA barrier; release is cumulative) before the
-// increment; acquire lets the last arriver's flag release cover every CTA's stores
-__device__ __forceinline__ uint32_t atom_add_acq_rel_sys(uint32_t* p, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.add.acq_rel.sys.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
 }
 
 __device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
@@ -172,16 +172,6 @@ __device__ __forceinline__ void red_add_v4(float* p, uint32_t a, uint32_t b, uin
                : "memory");
 }
 
-__device__ __forceinline__ uint64_t globaltimer_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-// generic-proxy smem writes -> visible to the async proxy (tcgen05.mma operand reads)
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 
 // ------------------------------------------------------------------ bulk copies (TMA)
 // 1-D bulk copy global -> shared, completion counted in bytes on `bar` (UBLKCP in SASS).
@@ -229,29 +219,12 @@ __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {  // whole warp
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
 }
 
-__device__ __forceinline__ void tmem_alloc_dyn(uint32_t* dst_smem, uint32_t cols) {  // whole warp
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
-               "r"(cols));
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-}
-
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {  // whole warp
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 inputs, fp32 accumulate), cta_group::1.
-__device__ __forceinline__ void umma_bf16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                             uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 
 // D[tmem] (+)= A[tmem] * B[smem]^T (A operand resident in tensor memory, K-major).
 __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
@@ -264,13 +237,6 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
       : "memory");
 }
 
-// thread i of the warp writes 8 consecutive 32-bit columns of TMEM lane (base lane + i)
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, uint4 a, uint4 b) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(a.x),
-               "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
-               : "memory");
-}
-
 // thread i of the warp writes 16 consecutive 32-bit columns of TMEM lane (base lane + i)
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, uint4 a, uint4 b, uint4 c, uint4 d) {
   asm volatile(
@@ -278,6 +244,18 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, uint4 a, uint4 b, uint
           taddr),
       "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w), "r"(c.x), "r"(c.y), "r"(c.z),
       "r"(c.w), "r"(d.x), "r"(d.y), "r"(d.z), "r"(d.w)
+      : "memory");
+}
+
+// thread i of the warp writes 32 consecutive 32-bit columns of TMEM lane (base lane + i)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint4 (&v)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0].x), "r"(v[0].y), "r"(v[0].z), "r"(v[0].w), "r"(v[1].x), "r"(v[1].y), "r"(v[1].z), "r"(v[1].w),
+      "r"(v[2].x), "r"(v[2].y), "r"(v[2].z), "r"(v[2].w), "r"(v[3].x), "r"(v[3].y), "r"(v[3].z), "r"(v[3].w),
+      "r"(v[4].x), "r"(v[4].y), "r"(v[4].z), "r"(v[4].w), "r"(v[5].x), "r"(v[5].y), "r"(v[5].z), "r"(v[5].w),
+      "r"(v[6].x), "r"(v[6].y), "r"(v[6].z), "r"(v[6].w), "r"(v[7].x), "r"(v[7].y), "r"(v[7].z), "r"(v[7].w)
       : "memory");
 }
 
@@ -344,18 +322,13 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(uint32_t M, uint32_t N) {
 // Bit 7 of word 0 (a sign-replicate bit whose two modes give the same result) flags rows
 // with >= 3 fallbacks, which take the rare patch path.
 
-// ------------------------------------------------------------------ row decoder, v2
-// Same contract as decode_row, restructured for the sm_100a issue budget:
-//   * the row's plane bytes arrive as the 32-bit plane halves w1..w3 (4 FragTile rows
-//     each); bsel = (r8 & 3) | 0x4440 extracts byte r8 zero-extended with one PRMT.
-//   * codewords are spread with integer multiplies (FMA pipe) instead of per-bit shifts:
-//     (b & 0xF) * K, K = 1 + 2^6 + 2^15 + 2^21, drops bits 0..3 on the LSBs of bytes
-//     0, 2, 1, 3 with no overlapping partial products (no carries), so
-//     WA = [c0, c2, c1, c3] and WB = [c4<<4, c6<<4, c5<<4, c7<<4] bytewise, and
-//       E0 = WA*128 + EB,  E1 = umulhi(WA, 2^31) + EB,  E2 = WB*8 + EB,  E3 = umulhi(WB, 2^27) + EB
-//     put (e_base + c) of elements (2j, 2j+1) on bits 7..14 / 23..30 of word j exactly;
-//     the garbage they also produce stays outside those bits (checked exhaustively).
-//   * the fallback PRMT selector is the high half of the table word (umulhi, FMA pipe).
+// Exponent assembly by multiply-spread (FMA pipe): (b & 0xF) * K, K = 1 + 2^6 + 2^15 + 2^21,
+// drops plane-byte bits 0..3 on the LSBs of bytes 0, 2, 1, 3 with no overlapping partial
+// products (no carries), so WA = [c0, c2, c1, c3] and WB = [c4<<4, c6<<4, c5<<4, c7<<4]
+// bytewise, and E0 = WA*128 + EB, E1 = umulhi(WA, 2^31) + EB, E2 = WB*8 + EB,
+// E3 = umulhi(WB, 2^27) + EB put (e_base + c) of elements (2j, 2j+1) on bits 7..14 / 23..30
+// of word j exactly; the garbage they also produce stays outside those bits (checked
+// exhaustively by the GPU parity tests on all 65,536 patterns).
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {  // all 4 selector bits
   uint32_t d;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
@@ -370,28 +343,12 @@ __device__ __forceinline__ uint32_t bitsel(uint32_t a, uint32_t b) {
   return d;
 }
 
-__device__ __forceinline__ uint32_t shfl_idx(uint32_t v, int src) {
-  uint32_t d;
-  asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(d) : "r"(v), "r"(src));
-  return d;
-}
-
 // Multipliers of the row decoder, read from constant memory so that ptxas keeps the
 // multiply-adds on the FMA pipe (with immediates it strength-reduces them to LEA / SHF,
 // which issue on the ALU pipe -- the decoder's bottleneck).
 #define ZS_KSPREAD (1u | (1u << 6) | (1u << 15) | (1u << 21))
-__constant__ uint32_t c_mul[16] = {1u << 28, 128u, 1u << 31, 8u, 1u << 27, 1u << 16, 0xFFFFFFFEu, 0xFFFFFFFFu,
-                                   ZS_KSPREAD, ZS_KSPREAD << 1, ZS_KSPREAD << 2, ZS_KSPREAD << 4,
-                                   ZS_KSPREAD << 5, ZS_KSPREAD << 6, 0u, 0u};
-#ifndef ZS_CMUL
-#define ZS_CMUL 1
-#endif
-#if ZS_CMUL
-#define ZS_MUL(idx, imm) c_mul[idx]
-#else
-#define ZS_MUL(idx, imm) (imm)
-#endif
-enum : int { kM28 = 0, kM7 = 1, kM31 = 2, kM3 = 3, kM27 = 4, kM16 = 5, kMNeg2 = 6, kMNeg1 = 7, kMK = 8, kMK4 = 11 };
+__constant__ uint32_t c_mul[8] = {1u << 28, 128u, 1u << 31, 8u, 1u << 27, 1u << 16, 0u, 0u};
+enum : int { kM28 = 0, kM7 = 1, kM31 = 2, kM3 = 3, kM27 = 4, kM16 = 5 };
 
 __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {  // a*b + c (FMA pipe)
   uint32_t d;
@@ -403,17 +360,6 @@ __device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
   asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   return d;
-}
-
-// Spread the 8 codeword bits of one plane byte b (bit i = element i) for WA / WB:
-//   lo = (b & 0xF) * K  and  hi = (b & 0xF0) * K, computed on the FMA pipe without the
-//   nibble masks: h4 = b >> 4 (= umulhi(b, 2^28)), hi = h4 * (K << 4), lo = b*K - hi.
-// kShift scales the plane (codeword bit k -> x2^k) through K.
-template <int kShift>
-__device__ __forceinline__ void spread_plane(uint32_t b, uint32_t& lo, uint32_t& hi) {
-  const uint32_t h4 = mad_hi(b, ZS_MUL(kM28, 1u << 28), 0u);
-  hi = mad_lo(h4, ZS_MUL(kMK4 + kShift, ZS_KSPREAD << (4 + kShift)), 0u);
-  lo = mad_lo(b, ZS_MUL(kMK + kShift, ZS_KSPREAD << kShift), mad_lo(hi, ZS_MUL(kMNeg1, 0xFFFFFFFFu), 0u));
 }
 
 // Row decoder on absolute smem pointers (the GEMM precomputes them):
@@ -442,81 +388,84 @@ __device__ __forceinline__ void patch_rank2(uint32_t m, const uint16_t* __restri
   }
 }
 
-__device__ __forceinline__ uint4 decode_row_abs(uint32_t b1, uint32_t b2, uint32_t b3, uint32_t m, uint4 ent,
-                                                const uint32_t* __restrict__ H32, uint32_t hsh8,
-                                                const uint16_t* __restrict__ Lrow, uint32_t eb7x2) {
-  const uint32_t h0 = H32[0], h1 = H32[1], h2 = H32[2];
-  const uint32_t hlo = __funnelshift_r(h0, h1, hsh8);
-  const uint32_t hhi = __funnelshift_r(h1, h2, hsh8);
-  // first two fallback values (FMA pipe: the ALU pipe is the decoder's bottleneck)
-  const uint32_t lpair = mad_lo(Lrow[1], ZS_MUL(kM16, 1u << 16), Lrow[0]);
+// ------------------------------------------------------------------ row decoder, v3 (GEMM)
+// decode_row_abs with every operand in registers: smem addresses as 32-bit shared-window
+// addresses (ld.shared with immediate offsets), the power-of-two multipliers of the
+// multiply-spread held in registers (loaded once per warp from c_mul, so ptxas cannot
+// strength-reduce the FMA-pipe multiplies into ALU shifts), the fallback-merge selector
+// taken from the high half of the table word with one IMAD.HI.
+struct DecConst {
+  uint32_t k28, k7, k31, k3, k27, k16, eb7x2;
+};
 
-  uint32_t l1, u1, l2, u2, l3, u3;
-  spread_plane<0>(b1, l1, u1);
-  spread_plane<1>(b2, l2, u2);
-  spread_plane<2>(b3, l3, u3);
-  // WA = [c0, c2, c1, c3], WB = [c4<<4, c6<<4, c5<<4, c7<<4] bytewise (see decode_row_w)
-  const uint32_t WA = (l1 & 0x01010101u) | (l2 & 0x02020202u) | (l3 & 0x04040404u);
-  const uint32_t WB = (u1 & 0x10101010u) | (u2 & 0x20202020u) | (u3 & 0x40404040u);
-  const uint32_t E[4] = {mad_lo(WA, ZS_MUL(kM7, 128u), eb7x2), mad_hi(WA, ZS_MUL(kM31, 1u << 31), eb7x2),
-                         mad_lo(WB, ZS_MUL(kM3, 8u), eb7x2), mad_hi(WB, ZS_MUL(kM27, 1u << 27), eb7x2)};
-  const uint32_t sel[4] = {ent.x, ent.y, ent.z, ent.w};
-  uint32_t out[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t P = prmt(hlo, hhi, sel[j]);                  // sign|mantissa bytes
-    const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);            // + exponent field
-    out[j] = prmt(lpair, w, mad_hi(sel[j], ZS_MUL(kM16, 1u << 16), 0u));      // fallback ranks 0/1
-  }
-  if (ent.x & 0x80u) patch_rank2(m, Lrow, out[0], out[1], out[2], out[3]);   // >= 3 fallbacks in the row: rare
-  return make_uint4(out[0], out[1], out[2], out[3]);
+__device__ __forceinline__ void load_dec_const(DecConst& d, uint32_t eb7x2) {
+  d.k28 = c_mul[kM28];
+  d.k7 = c_mul[kM7];
+  d.k31 = c_mul[kM31];
+  d.k3 = c_mul[kM3];
+  d.k27 = c_mul[kM27];
+  d.k16 = c_mul[kM16];
+  d.eb7x2 = eb7x2;
 }
 
-// Same as decode_row_abs with the fallback-merge selectors read from the table (fsel word j =
-// the high half of ent word j, pre-shifted) instead of extracted per word: 3 issue slots
-// fewer per row for one more 16-B table load.
-__device__ __forceinline__ uint4 decode_row_abs2(uint32_t b1, uint32_t b2, uint32_t b3, uint32_t m, uint4 ent,
-                                                 uint4 fsel, const uint32_t* __restrict__ H32, uint32_t hsh8,
-                                                 const uint16_t* __restrict__ Lrow, uint32_t eb7x2) {
-  const uint32_t h0 = H32[0], h1 = H32[1], h2 = H32[2];
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_shared_u16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
+// v = [a] if pred (v keeps its value otherwise): a predicated 16-B shared load, so lanes that
+// do not need the entry generate no shared-memory wavefront
+__device__ __forceinline__ void ld_shared_v4_if(uint4& v, uint32_t a, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %4, 0;\n\t"
+      "@p ld.shared.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}"
+      : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+      : "r"((uint32_t)pred), "r"(a));
+}
+
+template <int kShift>
+__device__ __forceinline__ void spread_plane_k(uint32_t b, const DecConst& d, uint32_t& lo, uint32_t& hi) {
+  const uint32_t h4 = mad_hi(b, d.k28, 0u);
+  hi = h4 * (ZS_KSPREAD << (4 + kShift));
+  lo = b * (ZS_KSPREAD << kShift) - hi;   // = (b & 0xF) * K: one IMAD with a negated addend
+}
+
+// haddr: shared address of the aligned word holding the row's first H byte; hsh8: 8 x that
+// byte's offset (low 5 bits used); laddr: shared address of the row's first fallback value.
+__device__ __forceinline__ uint4 decode_row_v3(uint32_t b1, uint32_t b2, uint32_t b3, uint4 ent, uint32_t haddr,
+                                               uint32_t hsh8, uint32_t laddr, const DecConst& d) {
+  const uint32_t h0 = ld_shared_u32(haddr), h1 = ld_shared_u32(haddr + 4), h2 = ld_shared_u32(haddr + 8);
   const uint32_t hlo = __funnelshift_r(h0, h1, hsh8);
   const uint32_t hhi = __funnelshift_r(h1, h2, hsh8);
-  // first two fallback values (FMA pipe: the ALU pipe is the decoder's bottleneck)
-  const uint32_t lpair = mad_lo(Lrow[1], ZS_MUL(kM16, 1u << 16), Lrow[0]);
+  const uint32_t lpair = mad_lo(ld_shared_u16(laddr + 2), d.k16, ld_shared_u16(laddr));
   uint32_t l1, u1, l2, u2, l3, u3;
-  spread_plane<0>(b1, l1, u1);
-  spread_plane<1>(b2, l2, u2);
-  spread_plane<2>(b3, l3, u3);
+  spread_plane_k<0>(b1, d, l1, u1);
+  spread_plane_k<1>(b2, d, l2, u2);
+  spread_plane_k<2>(b3, d, l3, u3);
   const uint32_t WA = (l1 & 0x01010101u) | (l2 & 0x02020202u) | (l3 & 0x04040404u);
   const uint32_t WB = (u1 & 0x10101010u) | (u2 & 0x20202020u) | (u3 & 0x40404040u);
-  const uint32_t E[4] = {mad_lo(WA, ZS_MUL(kM7, 128u), eb7x2), mad_hi(WA, ZS_MUL(kM31, 1u << 31), eb7x2),
-                         mad_lo(WB, ZS_MUL(kM3, 8u), eb7x2), mad_hi(WB, ZS_MUL(kM27, 1u << 27), eb7x2)};
+  const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), mad_hi(WA, d.k31, d.eb7x2), mad_lo(WB, d.k3, d.eb7x2),
+                         mad_hi(WB, d.k27, d.eb7x2)};
   const uint32_t sel[4] = {ent.x, ent.y, ent.z, ent.w};
-  const uint32_t fs[4] = {fsel.x, fsel.y, fsel.z, fsel.w};
   uint32_t out[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const uint32_t P = prmt(hlo, hhi, sel[j]);
     const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);
-    out[j] = prmt(lpair, w, fs[j]);
+    out[j] = prmt(lpair, w, mad_hi(sel[j], d.k16, 0u));
   }
-  if (ent.x & 0x80u) patch_rank2(m, Lrow, out[0], out[1], out[2], out[3]);   // >= 3 fallbacks in the row: rare
   return make_uint4(out[0], out[1], out[2], out[3]);
-}
-
-__device__ __forceinline__ uint4 decode_row_core(uint32_t b1, uint32_t b2, uint32_t b3, uint32_t m, uint4 ent,
-                                                 const uint8_t* __restrict__ H, uint32_t hs,
-                                                 const uint16_t* __restrict__ L, uint32_t ls, uint32_t eb7x2) {
-  return decode_row_abs(b1, b2, b3, m, ent, reinterpret_cast<const uint32_t*>(H + (hs & ~3u)), hs * 8u, L + ls,
-                        eb7x2);
-}
-
-// byte offset of FragTile o's 8-byte plane word inside a BlockTile plane that was loaded
-// by a 2-D TMA box {16 x u64, 4 TCT rows} with SWIZZLE_128B (1024-B aligned destination):
-// TCT row tr = o / 16 occupies 128 B whose 16-B chunks are XOR-permuted by tr.
-__device__ __forceinline__ uint32_t plane_off(uint32_t o) {
-  const uint32_t tr = o >> 4, j = o & 15u;
-  return tr * 128u + (((j >> 1) ^ tr) << 4) + ((j & 1u) << 3);
 }
 
 }  // namespace zs

@@ -44,21 +44,34 @@ namespace zs {
 // The SMSP arbiter issues from the highest eligible warp id first, so the latency-critical
 // single-warp roles take the TOP ids (a low-id producer / MMA warp starves behind six busy
 // decoder warps on its SMSP and the whole pipeline idles): decoders 0..23, epilogue 24..27.
-constexpr int kDecPerQuarter = 6;
-constexpr int kWarpDec0 = 0;                       // warps 0..23: decoders (lane quarter = warp % 4)
-constexpr int kWarpEpi0 = 4 * kDecPerQuarter;      // warps 24..27: epilogue (TMEM lane quarters)
-constexpr int kWarpAlloc = kWarpEpi0 + 4;          // 28
-constexpr int kWarpProdX = kWarpEpi0 + 5;          // 29
-constexpr int kWarpProdC = kWarpEpi0 + 6;          // 30
-constexpr int kWarpMma = kWarpEpi0 + 7;            // 31
-constexpr int kGemmThreads = 32 * (kWarpEpi0 + 8);  // 1024
+#ifndef ZS_PRED_SEL
+#define ZS_PRED_SEL 0   // 1: skip the selector-table load for all-in-window rows (predicated LDS)
+#endif
+#ifndef ZS_DEC_PER_Q
+#define ZS_DEC_PER_Q 4   // decoder warps per TMEM lane quarter (static unit assignment, see below)
+#endif
+constexpr int kDecPerQuarter = ZS_DEC_PER_Q;
+constexpr int kWarpDec0 = 0;                       // warps 0..4D-1: decoders (lane quarter = warp % 4)
+constexpr int kWarpEpi0 = 4 * kDecPerQuarter;      // 4 epilogue warps (TMEM lane quarters)
+constexpr int kWarpAlloc = kWarpEpi0 + 4;
+constexpr int kWarpProdX = kWarpEpi0 + 5;
+constexpr int kWarpProdC = kWarpEpi0 + 6;
+constexpr int kWarpMma = kWarpEpi0 + 7;            // highest id: first pick of its SMSP's arbiter
+constexpr int kGemmThreads = 32 * (kWarpEpi0 + 8);  // 768 at D = 4 (80 registers per thread)
 constexpr int kUPS = 4;                            // units per ring stage
-constexpr int kRowBatch = 4;                       // FragTile rows decoded together per thread
+#ifndef ZS_ROW_BATCH
+#define ZS_ROW_BATCH 4
+#endif
+constexpr int kRowBatch = ZS_ROW_BATCH;            // FragTile rows decoded together per thread
 constexpr int kMaxCSlots = 8;
 constexpr int kMaxXSlots = 16;
 constexpr int kMaxASlots = 12;
 constexpr uint32_t kStageMeta = 128;               // see the stage header layout below
-constexpr uint32_t kStagePlanes = 2 * 3 * kUPS * 512;
+// planes of a stage: [BlockTile row a | b][B1 | B2 | B3][unit][512 B]; row b's planes start
+// 32 B past a multiple of 128 B, so the two halves of a decoder warp (rows of BlockTile a and b
+// at the same FragTile position) read their plane bytes from different banks
+constexpr uint32_t kBtPlaneStride = 3 * kUPS * 512 + 32;
+constexpr uint32_t kStagePlanes = 2 * kBtPlaneStride;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kRpWarp = 32 * 16 + 32;          // per decoder warp: 32 FragTiles x 8 rows x u16 (+ pad)
 constexpr uint32_t kRpTabBytes = 4 * kDecPerQuarter * kRpWarp;
@@ -72,12 +85,11 @@ struct __align__(16) Bars {
   uint64_t xfull[kMaxXSlots / kUPS];     // per X-ring stage (4 tiles)
   uint64_t xempty[kMaxXSlots / kUPS];    // X stage consumed (tcgen05.commit after its last unit)
   uint64_t afree[kMaxASlots / kUPS];    // TMEM A stage free (tcgen05.commit after its MMAs)
+  uint64_t afull[kMaxASlots / kUPS];    // TMEM A stage decoded: one arrival per (unit, lane quarter)
   uint64_t accfull[2];
   uint64_t accempty[2];
   uint32_t tmem_base;
   uint32_t last_flag;
-  uint32_t tick[4];         // per TMEM lane quarter: next unit to decode (monotonic tickets)
-  alignas(16) uint32_t dcount[kMaxASlots];  // lane quarters decoded into A slot a (monotonic, +4 per use)
 };
 
 #ifndef ZS_REGSPLIT
@@ -122,26 +134,6 @@ __device__ __forceinline__ uint32_t bytepop(uint32_t x) {  // popcount of every 
   return (x + (x >> 4)) & 0x0F0F0F0Fu;
 }
 
-__device__ __forceinline__ void wait_count_eq(const uint32_t* ctr, uint32_t want) {
-  uint32_t n = 0;
-  while (ld_acquire_shared(ctr) != want) {
-    __nanosleep(32);
-    if (++n == (1u << 26)) zs_watchdog_fire(ctr, want);
-  }
-}
-
-__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
-  asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ void wait_count(const uint32_t* ctr, uint32_t need) {
-  uint32_t n = 0;
-  while (ld_acquire_shared(ctr) < need) {
-    __nanosleep(20);
-    if (++n == (1u << 26)) zs_watchdog_fire(ctr, need);
-  }
-}
-
 // fused exchange (f2): copy the mc outputs of one weight row n (column of Y), just stored
 // to the local Y by this thread, into every peer's Y.  Out of line, so the exchange adds no
 // register pressure to the rest of the kernel (it shares one 64-register allocation).
@@ -172,8 +164,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Bars* bars = reinterpret_cast<Bars*>(smem);
   uint8_t* rptab = smem + 1024;                        // decoder row-prefix tables
-  uint4* slut = reinterpret_cast<uint4*>(smem + 1024 + kRpTabBytes);   // PRMT selectors, 2 x 16 B per m
-  uint8_t* xslots = smem + 1024 + kRpTabBytes + 8192;
+  uint4* slut = reinterpret_cast<uint4*>(smem + 1024 + kRpTabBytes);   // PRMT selectors, 16 B per m
+  uint8_t* xslots = smem + 1024 + kRpTabBytes + 4096;
   uint8_t* cslots = xslots + (size_t)p.n_xslots * p.aslot_bytes;
 
   const int tid = threadIdx.x;
@@ -195,12 +187,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t band0 = u0 / nbc, kc0 = u0 % nbc;
 
   // ---- setup
-  if (tid < 256) {
-    const uint4 e = __ldg(&c_lut[tid]);
-    slut[2 * tid] = e;
-    slut[2 * tid + 1] = make_uint4(e.x >> 16, e.y >> 16, e.z >> 16, e.w >> 16);
-  }
-  if (tid < (int)p.n_cslots) reinterpret_cast<uint32_t*>(cslots + (size_t)tid * p.cslot_bytes)[24] = 0xFFFFFFFFu;
+  if (tid < 256) slut[tid] = __ldg(&c_lut[tid]);
   if (tid == 32) {
     for (uint32_t i = 0; i < S_c; ++i) {
       mbar_init(&bars->full_c[i], 1);
@@ -210,13 +197,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&bars->xfull[i], 1);
       mbar_init(&bars->xempty[i], 1);
     }
-    for (uint32_t i = 0; i < S_a; ++i) bars->dcount[i] = 0;
-    for (uint32_t i = 0; i < S_a / kUPS; ++i) mbar_init(&bars->afree[i], 1);
+    for (uint32_t i = 0; i < S_a / kUPS; ++i) {
+      mbar_init(&bars->afree[i], 1);
+      mbar_init(&bars->afull[i], 4 * kUPS);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->accfull[i], 1);
       mbar_init(&bars->accempty[i], 128);
     }
-    for (int i = 0; i < 4; ++i) bars->tick[i] = 0;
     fence_mbar_init();
   }
   if (warp == kWarpAlloc) tmem_alloc<kTmemCols>(&bars->tmem_base);
@@ -299,19 +287,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&bars->empty_c[slot], eph);
         uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
         const bool mine = (quad == st - b0 / kUPS);
-        if (mine && valid) {
+        // dbg & 8 (timing experiment): after the first ring fill the stages are not refilled;
+        // decoders re-decode the stale (self-consistent) slot contents -> decode without HBM
+        const bool stale = (p.dbg & 8) && st >= (int)S_c;
+        if (mine && valid && !stale) {
           uint32_t* meta = reinterpret_cast<uint32_t*>(cs);
           *reinterpret_cast<uint4*>(meta + 4 * qi) = make_uint4(oha, ohb, ola, olb);
           meta[20 + qi] = has_b ? 1u : 0u;
-          if (qi == 0) meta[24] = (uint32_t)st;   // generation: the stage this slot now holds
         }
         __syncwarp();
-        if (mine && qi == 0) {
+        if (mine && qi == 0 && stale) mbar_arrive(&bars->full_c[slot]);
+        if (mine && qi == 0 && !stale) {
           mbar_arrive_expect_tx(&bars->full_c[slot], stage_bytes);  // release: header visible
           trace_ev(p.trace, it, 0);
         }
         __syncwarp();
-        if (mine && run_start) {
+        if (mine && run_start && !stale) {
           uint64_t* fb = &bars->full_c[slot];
           uint8_t* planes = cs + kStageMeta;
           uint8_t* Hr = planes + kStagePlanes;   // [H a | H b | L a | L b]
@@ -325,9 +316,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             bulk_g2s(Hr + 2 * capH + ola, reinterpret_cast<const uint8_t*>(p.l) + l0a, e_l1a - l0a, fb, pol);
           if (has_b) {
             const size_t btb = (size_t)bta + nbc;
-            bulk_g2s(planes + 3 * (kUPS * 512) + po, p.b1 + btb * 64, pb, fb, pol);
-            bulk_g2s(planes + 4 * (kUPS * 512) + po, p.b2 + btb * 64, pb, fb, pol);
-            bulk_g2s(planes + 5 * (kUPS * 512) + po, p.b3 + btb * 64, pb, fb, pol);
+            bulk_g2s(planes + kBtPlaneStride + 0 * (kUPS * 512) + po, p.b1 + btb * 64, pb, fb, pol);
+            bulk_g2s(planes + kBtPlaneStride + 1 * (kUPS * 512) + po, p.b2 + btb * 64, pb, fb, pol);
+            bulk_g2s(planes + kBtPlaneStride + 2 * (kUPS * 512) + po, p.b3 + btb * 64, pb, fb, pol);
             if (e_h1b > h0b) bulk_g2s(Hr + capH + ohb, p.h + h0b, e_h1b - h0b, fb, pol);
             if (e_l1b > l0b)
               bulk_g2s(Hr + 2 * capH + capL + olb, reinterpret_cast<const uint8_t*>(p.l) + l0b, e_l1b - l0b, fb,
@@ -386,20 +377,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     };
     uint32_t xs = 0, xph = 0;                     // X stage ring slot / parity
-    uint32_t as_ = 0, need = 4;                   // A stage ring / decoded count each slot needs
+    uint32_t as_ = 0, aph = 0;                    // A stage ring slot / parity of its afull phase
     uint32_t xa = xbase, ta = tmem_a;             // X tile address / A slot column of the stage
     const uint32_t xa_end = xbase + S_x * p.aslot_bytes, ta_end = tmem_a + 32u * S_a;
     for (int st = 0; st < nstages; ++st) {
       const int i0 = st * kUPS, nu = min(kUPS, nunits - i0);
       mbar_wait(&bars->xfull[xs], xph);
       try_signal();
-      for (int j = 0; j < nu; ++j) {
-        const uint32_t* c = &bars->dcount[as_ * kUPS + j];
-        uint32_t n = 0;
-        while (ld_acquire_shared(c) < need) {
-          if (++n == (1u << 28)) zs_watchdog_fire(c, need);
-        }
-      }
+      mbar_wait(&bars->afull[as_], aph);          // all 4 x 4 unit-quarters of the stage decoded
       tc_fence_after();
       if (nu == kUPS && i0 != 0 && i0 + kUPS < nunits && kc != 0 && kc + kUPS < nbc) {
         // fast path: a full stage strictly inside one accumulation segment -> 16 MMAs from
@@ -464,7 +449,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           ta += 32u * (uint32_t)(kUPS - nu); if (ta >= ta_end) ta -= ta_end - tmem_a;
         }
       }
-      if (++as_ == SAS) { as_ = 0; need += 4; }
+      if (++as_ == SAS) { as_ = 0; aph ^= 1u; }
       if (++xs == SXS) { xs = 0; xph ^= 1u; }
     }
     // the last segment(s): wait for their accumulators, then wake the epilogue
@@ -475,140 +460,167 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp < kWarpEpi0) {
     // ================================================================ decoders
+    // Static assignment: decoder warp jd (0..D-1) of TMEM lane quarter q decodes quarter q
+    // of the CTA's units jd, jd + D, jd + 2D, ... in order.  The D warps of a quarter issue at
+    // the same rate on one SMSP (no tickets), and a warp that visits its stages in order cannot
+    // see a stale ring phase (its previous unit's stage was filled after the slot's older fill).
+    //
+    // Lane -> weight row: quarter q = half hh = q & 1 of BlockTile row bt = q >> 1; lane t holds
+    // row 32 hh + t of that BlockTile, so the warp's 32 FragTiles (TCT rows 2hh, 2hh + 1) are
+    // contiguous in canonical order and its scan needs only the first half's total.
     const int q = warp & 3;                       // TMEM lane quarter (== warp % 4)
-    const int bt_sel = q >> 1, hh = q & 1;
+    const int jd = (warp - kWarpDec0) >> 2;       // decoder index inside the quarter
+    const int bt = q >> 1, hh = q & 1;
     const int lr = lane + 32 * hh;                // row inside the BlockTile
     const int fr = lr >> 3, r8 = lr & 7;
     const int tr = fr >> 1;                       // TensorCoreTile row of this thread's FragTiles
     const uint32_t obase = (uint32_t)(tr * 16 + (fr & 1));                 // o for fc = 0
     const uint32_t tq = tmem_a + ((uint32_t)(32 * q) << 16);
     const int fo = 32 * hh + lane;                // scan lane's FragTile
-    // row-prefix table of this warp: FragTile o (local 0..31) at o*8 + (o >> 4)*16 (the pad
-    // keeps the 4 FragTiles a warp reads at once on distinct banks)
     uint8_t* rpt = rptab + (warp - kWarpDec0) * kRpWarp;
     // row table: FragTile o (local 0..31) at o*16 + (o >> 4)*32 bytes, row r8 at + 2*r8 (the
     // pad keeps the 4 FragTiles a warp reads at once on distinct banks)
     const uint32_t rp_wr = (uint32_t)lane * 16u + ((uint32_t)lane >> 4) * 32u;
     const uint32_t ol0 = obase - 32u * hh;        // local FragTile index for fc = 0
-    // Tickets: the warps of a quarter take units from one monotonic counter, so no warp idles
-    // while a loaded unit is waiting (a stage holds kUPS units, 4 x kUPS unit-quarters).
-    while (true) {
-      uint32_t u = 0;
-      if (lane == 0) u = atomicAdd(&bars->tick[q], 1u);
-      u = shfl_idx(u, 0);
-      if ((int)u >= nunits) break;
-      if (lane == 0 && q < 2) trace_ev(p.trace, (int)u, q == 0 ? 1 : 15);   // ticket drawn
-      const int st = (int)(u / kUPS);
-      const uint32_t j = u % kUPS;
-      const uint32_t stc = fastdiv((uint32_t)st, S_c, p.cdiv_magic);
-      const uint32_t slot = (uint32_t)st - stc * S_c, cph = stc & 1u;
-      const uint32_t SAS = S_a / kUPS;
-      const uint32_t ag = fastdiv((uint32_t)st, SAS, p.adiv_magic);  // use count of the A stage
-      const uint32_t astg = (uint32_t)st - ag * SAS;                 // TMEM A stage of this unit
-      const uint32_t a = astg * kUPS + j;                            // TMEM A slot of this unit
+    const uint32_t rb_off = ol0 * 16u + (ol0 >> 4) * 32u + 2u * (uint32_t)r8;
+    const uint32_t SAS = S_a / kUPS;
+    DecConst dk;
+    load_dec_const(dk, p.eb7x2);
+    const uint32_t slut_b = smem_u32(slut);
+    const uint32_t sbase = smem_u32(smem);
+    for (int u = jd; u < nunits; u += kDecPerQuarter) {
+      const uint32_t st = (uint32_t)u / kUPS, j = (uint32_t)u % kUPS;
+      const uint32_t stc = fastdiv(st, S_c, p.cdiv_magic);
+      const uint32_t slot = st - stc * S_c, cph = stc & 1u;
+      const uint32_t ag = fastdiv(st, SAS, p.adiv_magic);  // use count of the A stage
+      const uint32_t astg = st - ag * SAS;                 // TMEM A stage of this unit
+      const uint32_t a = astg * kUPS + j;                  // TMEM A slot of this unit
       const uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
       const uint32_t* meta = reinterpret_cast<const uint32_t*>(cs);
-      // The slot's header names the stage it holds (meta[24]); once it names st, the parity
-      // wait below cannot alias an older fill.
-      if (ld_acquire_shared(meta + 24) != (uint32_t)st || !mbar_test_wait(&bars->full_c[slot], cph)) {
-        wait_count_eq(meta + 24, (uint32_t)st);
-        mbar_wait(&bars->full_c[slot], cph);
+      mbar_wait(&bars->full_c[slot], cph);
+      if (lane == 0) trace_ev(p.trace, u, 7 + q);
+      // an absent BlockTile row b (odd row count) is aliased to row a: its rows decode valid
+      // bytes into TMEM lanes whose outputs (rows >= N) the epilogue never stores
+      const int btx = (bt == 1 && meta[20 + j] != 0u) ? 1 : 0;
+      const uint4 mt = *reinterpret_cast<const uint4*>(meta + 4 * j);  // {H a, H b, L a, L b}
+      const uint8_t* P1 = cs + kStageMeta + btx * kBtPlaneStride + j * 512;
+      const uint8_t* P2 = P1 + kUPS * 512;
+      const uint8_t* P3 = P2 + kUPS * 512;
+      const uint8_t* Hr = cs + kStageMeta + kStagePlanes;
+      const uint8_t* H = Hr + btx * capH + (btx ? mt.y : mt.x);
+      const uint8_t* L = Hr + 2 * capH + btx * capL + (btx ? mt.w : mt.z);
+      // ---- scan: lane = FragTile 32*hh + lane (canonical order)
+      const uint2 s1 = *reinterpret_cast<const uint2*>(P1 + fo * 8);
+      const uint2 s2 = *reinterpret_cast<const uint2*>(P2 + fo * 8);
+      const uint2 s3 = *reinterpret_cast<const uint2*>(P3 + fo * 8);
+      const uint32_t mlo = s1.x | s2.x | s3.x, mhi = s1.y | s2.y | s3.y;
+      const uint32_t cnt = __popc(mlo) + __popc(mhi);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += t;
       }
-      {
-        const int it = (int)u;
-        const bool present = (bt_sel == 0) || (meta[20 + j] != 0u);
-        if (lane == 0) trace_ev(p.trace, it, 7 + q);
-        if (present) {
-          const uint4 mt = *reinterpret_cast<const uint4*>(meta + 4 * j);  // {H a, H b, L a, L b}
-          const uint8_t* P1 = cs + kStageMeta + (bt_sel * 3) * (kUPS * 512) + j * 512;
-          const uint8_t* P2 = P1 + kUPS * 512;
-          const uint8_t* P3 = P2 + kUPS * 512;
-          const uint8_t* Hr = cs + kStageMeta + kStagePlanes;
-          const uint8_t* H = Hr + bt_sel * capH + (bt_sel ? mt.y : mt.x);
-          const uint16_t* L =
-              reinterpret_cast<const uint16_t*>(Hr + 2 * capH + bt_sel * capL + (bt_sel ? mt.w : mt.z));
-          // ---- scan: lane = FragTile 32*hh + lane (canonical order)
-          const uint2 s1 = *reinterpret_cast<const uint2*>(P1 + fo * 8);
-          const uint2 s2 = *reinterpret_cast<const uint2*>(P2 + fo * 8);
-          const uint2 s3 = *reinterpret_cast<const uint2*>(P3 + fo * 8);
-          const uint32_t mlo = s1.x | s2.x | s3.x, mhi = s1.y | s2.y | s3.y;
-          const uint32_t cnt = __popc(mlo) + __popc(mhi);
-          uint32_t incl = cnt;
+      uint32_t excl = incl - cnt;
+      if (hh) {
+        const uint2 t1 = *reinterpret_cast<const uint2*>(P1 + lane * 8);
+        const uint2 t2 = *reinterpret_cast<const uint2*>(P2 + lane * 8);
+        const uint2 t3 = *reinterpret_cast<const uint2*>(P3 + lane * 8);
+        excl += __reduce_add_sync(0xFFFFFFFFu, __popc(t1.x | t2.x | t3.x) + __popc(t1.y | t2.y | t3.y));
+      }
+      // H byte offset (from this BlockTile's H base) of each of the FragTile's 8 rows, u16
+      const uint32_t bl = bytepop(mlo), bh = bytepop(mhi);
+      const uint32_t rp_lo = bl * 0x01010100u;
+      const uint32_t rp_hi = bh * 0x01010100u + ((bl * 0x01010101u) >> 24) * 0x01010101u;
+      const uint32_t ex2 = excl * 0x10001u;
+      const uint4 hrow = make_uint4(prmt(rp_lo, 0u, 0x4140u) + ex2, prmt(rp_lo, 0u, 0x4342u) + ex2,
+                                    prmt(rp_hi, 0u, 0x4140u) + ex2, prmt(rp_hi, 0u, 0x4342u) + ex2);
+      __syncwarp();   // previous unit's readers are done
+      *reinterpret_cast<uint4*>(rpt + rp_wr) = hrow;
+      __syncwarp();
+      // the slot is free once the MMAs of stage st - SAS have completed (their commit)
+      if (ag > 0) mbar_wait(&bars->afree[astg], (ag - 1u) & 1u);
+      tc_fence_after();
+      const uint32_t taddr0 = tq + 32u * a;
+      // per-row addresses = a per-unit base + an immediate.  FragTile of row f: o = obase +
+      // cf(f), cf(f) = (f>>1)*4 + (f&1)*2 (canonical order of FragTile column f).
+      const uint8_t* pb = P1 + obase * 8u + (uint32_t)r8;           // this row's plane byte, f = 0
+      const uint8_t* rb = rpt + rb_off;
+      const uint32_t hb = (uint32_t)(H - smem);                     // 16-B aligned
+      // fallback values of row f start at element 8*(o*8 + r8) - (its H offset) of the unit's L
+      const uint32_t la0 = (uint32_t)(L - smem) + 2u * hb + 16u * (obase * 8u + (uint32_t)r8);
+      uint32_t rare = 0;
 #pragma unroll
-          for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-            if (lane >= d) incl += t;
+      for (int fb = 0; fb < 8; fb += kRowBatch) {
+        if (p.dbg & 1) break;
+        uint4 v[kRowBatch];
+#pragma unroll
+        for (int qq = 0; qq < kRowBatch; ++qq) {
+          const int f = fb + qq;
+          const uint32_t cf = (uint32_t)((f >> 1) * 4 + (f & 1) * 2);
+          const uint32_t hs_abs = hb + *reinterpret_cast<const uint16_t*>(rb + cf * 16u);
+          const uint32_t b1 = pb[cf * 8u];
+          const uint32_t b2 = pb[cf * 8u + kUPS * 512];
+          const uint32_t b3 = pb[cf * 8u + 2 * kUPS * 512];
+          const uint32_t m = b1 | b2 | b3;
+#if ZS_PRED_SEL
+          // the all-in-window row (m = 0xFF, ~84% at sigma = 0.02) takes the constant entry
+          uint4 ent = make_uint4(0x76549100u, 0x7654B3A2u, 0x7654D5C4u, 0x7654F7E6u);
+          ld_shared_v4_if(ent, slut_b + m * 16u, m != 0xFFu);
+#else
+          const uint4 ent = ld_shared_v4(slut_b + m * 16u);
+#endif
+          rare |= ent.x;
+          v[qq] = decode_row_v3(b1, b2, b3, ent, sbase + (hs_abs & ~3u), hs_abs * 8u,
+                                sbase + la0 + 128u * cf - 2u * hs_abs, dk);
+        }
+        if (__any_sync(0xFFFFFFFFu, rare & 0x80u)) {
+          // rare: a row of this batch has >= 3 fallbacks (rank >= 2); warp-uniform branch
+#pragma unroll
+          for (int qq = 0; qq < kRowBatch; ++qq) {
+            const int f = fb + qq;
+            const uint32_t cf = (uint32_t)((f >> 1) * 4 + (f & 1) * 2);
+            const uint32_t hs_abs = hb + *reinterpret_cast<const uint16_t*>(rb + cf * 16u);
+            const uint32_t m = pb[cf * 8u] | pb[cf * 8u + kUPS * 512] | pb[cf * 8u + 2 * kUPS * 512];
+            if (slut[m].x & 0x80u)
+              patch_rank2(m, reinterpret_cast<const uint16_t*>(smem + la0 + 128u * cf - 2u * hs_abs), v[qq].x,
+                          v[qq].y, v[qq].z, v[qq].w);
           }
-          uint32_t excl = incl - cnt;
-          if (hh) {
-            const uint2 t1 = *reinterpret_cast<const uint2*>(P1 + lane * 8);
-            const uint2 t2 = *reinterpret_cast<const uint2*>(P2 + lane * 8);
-            const uint2 t3 = *reinterpret_cast<const uint2*>(P3 + lane * 8);
-            excl += __reduce_add_sync(0xFFFFFFFFu, __popc(t1.x | t2.x | t3.x) + __popc(t1.y | t2.y | t3.y));
-          }
-          // H start of each of the FragTile's 8 rows (relative to the unit's H base), u16
-          const uint32_t bl = bytepop(mlo), bh = bytepop(mhi);
-          const uint32_t rp_lo = bl * 0x01010100u;
-          const uint32_t rp_hi = bh * 0x01010100u + ((bl * 0x01010101u) >> 24) * 0x01010101u;
-          const uint32_t ex2 = excl * 0x10001u;
-          const uint4 hrow = make_uint4(prmt(rp_lo, 0u, 0x4140u) + ex2, prmt(rp_lo, 0u, 0x4342u) + ex2,
-                                        prmt(rp_hi, 0u, 0x4140u) + ex2, prmt(rp_hi, 0u, 0x4342u) + ex2);
-          __syncwarp();   // previous unit's readers are done
-          *reinterpret_cast<uint4*>(rpt + rp_wr) = hrow;
-          __syncwarp();
-          // the slot is free once the MMAs of stage st - SAS have completed (their commit)
-          if (ag > 0) mbar_wait(&bars->afree[astg], (ag - 1u) & 1u);
-          tc_fence_after();
-          if (lane == 0) trace_ev(p.trace, it, 11 + q);
-          const uint32_t taddr0 = tq + 32u * a;
-          // Absolute smem byte offsets (relative to `smem`) so every per-row address is a
-          // per-unit base plus an immediate.  FragTile of row f: o = obase + cf(f),
-          // cf(f) = (f>>1)*4 + (f&1)*2 (canonical order of FragTile column f).
-          const uint32_t hb = (uint32_t)(H - smem);                     // 16-B aligned
-          const uint8_t* pb = P1 + obase * 8u + (uint32_t)r8;           // this row's plane byte, f = 0
-          const uint8_t* rb = rpt + ol0 * 16u + (ol0 >> 4) * 32u + 2u * (uint32_t)r8;
-          const uint32_t la0 = (uint32_t)((const uint8_t*)L - smem) + 2u * hb +
-                               16u * (obase * 8u + (uint32_t)r8);      // + 128 cf(f) - 2 hs_abs
+        }
+        rare = 0;
+        if (p.dbg & 2) {
+          uint32_t x = 0;
 #pragma unroll
-          for (int fb = 0; fb < 8; fb += kRowBatch) {
-            if (p.dbg & 1) break;
-            uint4 v[kRowBatch];
-#pragma unroll
-            for (int qq = 0; qq < kRowBatch; ++qq) {
-              const int f = fb + qq;
-              const uint32_t cf = (uint32_t)((f >> 1) * 4 + (f & 1) * 2);
-              const uint32_t hs_abs = hb + *reinterpret_cast<const uint16_t*>(rb + cf * 16u);
-              const uint32_t b1 = pb[cf * 8u];
-              const uint32_t b2 = pb[cf * 8u + kUPS * 512];
-              const uint32_t b3 = pb[cf * 8u + 2 * kUPS * 512];
-              const uint32_t m = b1 | b2 | b3;
-              v[qq] = decode_row_abs2(b1, b2, b3, m, slut[2 * m], slut[2 * m + 1],
-                                     reinterpret_cast<const uint32_t*>(smem + (hs_abs & ~3u)), hs_abs * 8u,
-                                     reinterpret_cast<const uint16_t*>(smem + mad_lo(hs_abs, ZS_MUL(kMNeg2, 0xFFFFFFFEu), la0 + 128u * cf)),
-                                     p.eb7x2);
-            }
-            if (p.dbg & 2) {
-              uint32_t x = 0;
-#pragma unroll
-              for (int qq = 0; qq < kRowBatch; ++qq) x ^= v[qq].x ^ v[qq].y ^ v[qq].z ^ v[qq].w;
-              if (x == 0x9E3779B9u) p.counters[0] = x;   // keeps the decode live
-            } else {
-              tmem_st16(taddr0 + 4u * fb, v[0], v[1], v[2], v[3]);   // one 16-column store per 4 rows
-            }
-          }
-          // publish the unit-quarter at once (the MMA warp spins on the slot's counter)
-          tmem_wait_st();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) red_release_add(&bars->dcount[a], 1u);
-          if (lane == 0) trace_ev(p.trace, it, 2 + q);
-        } else {   // absent BlockTile row b (odd row count): nothing to decode
-          if (ag > 0) mbar_wait(&bars->afree[astg], (ag - 1u) & 1u);
-          if (lane == 0) red_release_add(&bars->dcount[a], 1u);
+          for (int qq = 0; qq < kRowBatch; ++qq) x ^= v[qq].x ^ v[qq].y ^ v[qq].z ^ v[qq].w;
+          if (x == 0x9E3779B9u) p.counters[0] = x;   // keeps the decode live
+        } else {
+#if ZS_ROW_BATCH == 8
+          tmem_st32(taddr0, v);
+#else
+          tmem_st16(taddr0 + 4u * fb, v[0], v[1], v[2], v[3]);   // one 16-column store per 4 rows
+#endif
         }
       }
+      // publish the unit-quarter (release: the MMA warp's acquire on afull orders its MMAs
+      // after these TMEM stores)
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->afull[astg]);
+      if (lane == 0) trace_ev(p.trace, u, 2 + q);
       __syncwarp();                                    // all lanes done reading the stage
       if (lane == 0) mbar_arrive(&bars->empty_c[slot]);
+    }
+    // A partial last stage still needs its 16 afull arrivals: this warp's units past the end
+    // that fall in that stage arrive without decoding (after the slot's previous use is
+    // retired, so the arrival lands in the right phase).
+    for (int u = jd + ((nunits - jd + kDecPerQuarter - 1) / kDecPerQuarter) * kDecPerQuarter;
+         u < nstages * kUPS; u += kDecPerQuarter) {
+      const uint32_t st = (uint32_t)u / kUPS;
+      const uint32_t ag = fastdiv(st, SAS, p.adiv_magic), astg = st - ag * SAS;
+      if (ag > 0) mbar_wait(&bars->afree[astg], (ag - 1u) & 1u);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->afull[astg]);
     }
   } else if (warp < kWarpEpi0 + 4) {
     // ================================================================ epilogue (warps 4..7)
@@ -729,7 +741,7 @@ cudaError_t launch_gemm(const GemmParams& p, const CUtensorMap& xmap, int grid, 
 }
 
 size_t gemm_smem_bytes(const GemmParams& p) {
-  return 1024 /*align slack*/ + 1024 + kRpTabBytes + 8192 + (size_t)p.n_xslots * p.aslot_bytes +
+  return 1024 /*align slack*/ + 1024 + kRpTabBytes + 4096 + (size_t)p.n_xslots * p.aslot_bytes +
          (size_t)p.n_cslots * p.cslot_bytes;
 }
 
@@ -740,6 +752,6 @@ int gemm_max_aslots() { return kMaxASlots; }
 uint32_t gemm_stage_fixed_bytes() { return kStageMeta + kStagePlanes; }
 int gemm_units_per_stage() { return kUPS; }
 int gemm_max_chunk() { return 128; }
-uint32_t gemm_fixed_smem() { return 1024 + 1024 + kRpTabBytes + 8192; }
+uint32_t gemm_fixed_smem() { return 1024 + 1024 + kRpTabBytes + 4096; }
 
 }  // namespace zs

@@ -60,10 +60,10 @@ __global__ void peer_wait_kernel(const uint32_t* flags, int n, uint32_t epoch, u
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int i = threadIdx.x;
   if (i < n) {
-    const uint64_t t0 = globaltimer_ns();
+    const uint64_t t0 = globaltimer_now();
     while ((int32_t)(ld_acquire_sys(flags + i) - epoch) < 0) {
       __nanosleep(256);
-      if (globaltimer_ns() - t0 > timeout_ns) {
+      if (globaltimer_now() - t0 > timeout_ns) {
         printf("zs_peer_wait: flag %d = %u never reached epoch %u\n", i, ld_acquire_sys(flags + i), epoch);
         __trap();
       }

@@ -12,9 +12,11 @@ l2 = torch.cuda.get_device_properties(dev).L2_cache_size
 layers = (sys.argv[1] if len(sys.argv) > 1 else "L8B.GateUp").split(",")
 FLAGS = [int(f) for f in (sys.argv[2] if len(sys.argv) > 2 else "0,4,2,6,1,5").split(",")]
 MS = [int(m) for m in (sys.argv[3] if len(sys.argv) > 3 else "1,32").split(",")]
+DIST = sys.argv[sys.argv.index("--dist") + 1] if "--dist" in sys.argv else "gaussian"
 for layer in layers:
   K, N = G.LAYERS[layer]
-  zh = Z.encode(G.gaussian_bf16(N, K, 0.02, G.seed_of(layer)))
+  gen = G.realistic_bf16 if DIST == "realistic" else G.gaussian_bf16
+  zh = Z.encode(gen(N, K, 0.02, seed=G.seed_of(layer)))
   R = max(2, math.ceil(3 * l2 / zh.nbytes()))
   comp = [zh.to(dev) for _ in range(R)]
   for M in MS:
@@ -33,6 +35,6 @@ for layer in layers:
             Z.gemm(x, comp[i % R], out=y, ws=ws)
         e1.record()
         torch.cuda.synchronize()
-        print(json.dumps({"layer": layer, "mb": round(zh.nbytes() / 1e6, 1), "M": M, "flags": flags, "us": round(e0.elapsed_time(e1) * 1e3 / n, 2)}), flush=True)
+        print(json.dumps({"layer": layer, "mb": round(zh.nbytes() / 1e6, 1), "M": M, "flags": flags, "dist": DIST, "us": round(e0.elapsed_time(e1) * 1e3 / n, 2)}), flush=True)
     L.zs_debug_set_flags(0)
     ws.zero_()
