@@ -83,18 +83,16 @@ __device__ __forceinline__ uint64_t globaltimer_now() {
   return t;
 }
 
-// Wait for the phase with the given parity.  After one plain probe the waiting warp is
-// suspended in hardware (try_wait with a time hint: it resumes when the phase completes),
-// so a waiting role costs no issue slots on the SMSP it shares with decoder warps.  The
-// watchdog is time based (checked every 256 suspended probes): > 10 s traps.
-static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity);
+// Wait for the phase with the given parity.  After one probe the waiting warp backs off with
+// nanosleep between probes: a waiting warp shares its SMSP with decoder warps (and the arbiter
+// favours high warp ids, i.e. the control warps), so a tight polling loop would take their
+// issue slots.  The watchdog is time based (checked every 256 probes): > 10 s traps.
+static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity, uint32_t backoff_ns);
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t backoff_ns = 64) {
+  if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity, backoff_ns);
 }
 
-// for idle roles (epilogue): try_wait with a suspend-time hint -- the warp is descheduled
-// (no issue slots) until the phase completes or ~the hint elapses
 __device__ __forceinline__ bool mbar_try_wait_suspend(uint64_t* bar, uint32_t parity, uint32_t ns) {
   uint32_t ok;
   asm volatile(
@@ -107,9 +105,10 @@ __device__ __forceinline__ bool mbar_try_wait_suspend(uint64_t* bar, uint32_t pa
   return ok != 0;
 }
 
-static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
+static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity, uint32_t backoff_ns) {
   uint64_t t0 = 0;
-  for (uint32_t n = 1; !mbar_try_wait_suspend(bar, parity, 0x100000u); ++n) {
+  for (uint32_t n = 1; !mbar_try_wait(bar, parity); ++n) {
+    __nanosleep(backoff_ns);
     if ((n & 255u) == 0u) {
       const uint64_t t = globaltimer_now();
       if (t0 == 0) t0 = t;
@@ -259,6 +258,17 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint4 (&v)[8]) {
       : "memory");
 }
 
+// 16 TMEM lanes (base lane + t, t = lane & 15), two column blocks: threads 0..15 write columns
+// [c, c+16) of their lane, threads 16..31 columns [c+16, c+32) of the SAME lanes
+__device__ __forceinline__ void tmem_st16x2(uint32_t taddr, uint4 a, uint4 b, uint4 c, uint4 d) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x32bx2.x16.b32 [%0], 16, {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::
+          "r"(taddr),
+      "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w), "r"(c.x), "r"(c.y), "r"(c.z),
+      "r"(c.w), "r"(d.x), "r"(d.y), "r"(d.z), "r"(d.w)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete
@@ -356,6 +366,12 @@ __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
   return d;
 }
 
+__device__ __forceinline__ uint32_t mul_hi(uint32_t a, uint32_t b) {  // hi(a*b) (FMA pipe, quarter rate)
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {  // hi(a*b) + c (FMA pipe)
   uint32_t d;
   asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
@@ -434,36 +450,121 @@ __device__ __forceinline__ void ld_shared_v4_if(uint4& v, uint32_t a, bool pred)
       : "r"((uint32_t)pred), "r"(a));
 }
 
+// Spread of one plane byte b (bit i = element i) into WA / WB positions:
+//   lo = (b & 0xF) * K  and  hi = (b & 0xF0) * K = b * K - lo   (K shifted by the plane's weight)
+// one LOP3 + two full-rate IMADs; no IMAD.HI (a quarter-rate instruction on sm_100a:
+// 0.24 vs 0.5 warp-instructions / cycle / SMSP, scripts/pipe_probe.cu)
+#ifndef ZS_DEC_BAL
+// Pipe balance of the row decoder (sm_100a: LOP3 / PRMT / SHF and IMAD issue at 0.5 warp-instr
+// per cycle per SMSP, IMAD.HI at 0.24; scripts/pipe_probe.cu).  2: shifts split between the
+// FMA pipe (IMAD.HI) and the ALU pipe (SHF) so both pipes carry about the same cycles per row;
+// 1: all shifts on the FMA pipe; 0: all shifts on the ALU pipe.
+#define ZS_DEC_BAL 2
+#endif
 template <int kShift>
 __device__ __forceinline__ void spread_plane_k(uint32_t b, const DecConst& d, uint32_t& lo, uint32_t& hi) {
-  const uint32_t h4 = mad_hi(b, d.k28, 0u);
-  hi = h4 * (ZS_KSPREAD << (4 + kShift));
-  lo = b * (ZS_KSPREAD << kShift) - hi;   // = (b & 0xF) * K: one IMAD with a negated addend
+#if ZS_DEC_BAL
+  hi = mul_hi(b, d.k28) * (ZS_KSPREAD << (4 + kShift));   // (b >> 4) on the FMA pipe
+  lo = b * (ZS_KSPREAD << kShift) - hi;
+#else
+  lo = (b & 0xFu) * (ZS_KSPREAD << kShift);
+  hi = b * (ZS_KSPREAD << kShift) - lo;
+#endif
 }
 
 // haddr: shared address of the aligned word holding the row's first H byte; hsh8: 8 x that
 // byte's offset (low 5 bits used); laddr: shared address of the row's first fallback value.
+__device__ __forceinline__ uint2 ld_shared_v2(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+
 __device__ __forceinline__ uint4 decode_row_v3(uint32_t b1, uint32_t b2, uint32_t b3, uint4 ent, uint32_t haddr,
                                                uint32_t hsh8, uint32_t laddr, const DecConst& d) {
   const uint32_t h0 = ld_shared_u32(haddr), h1 = ld_shared_u32(haddr + 4), h2 = ld_shared_u32(haddr + 8);
   const uint32_t hlo = __funnelshift_r(h0, h1, hsh8);
   const uint32_t hhi = __funnelshift_r(h1, h2, hsh8);
+#if ZS_DEC_BAL
   const uint32_t lpair = mad_lo(ld_shared_u16(laddr + 2), d.k16, ld_shared_u16(laddr));
+#else
+  const uint32_t lpair = prmt(ld_shared_u16(laddr), ld_shared_u16(laddr + 2), 0x5410u);
+#endif
   uint32_t l1, u1, l2, u2, l3, u3;
   spread_plane_k<0>(b1, d, l1, u1);
   spread_plane_k<1>(b2, d, l2, u2);
   spread_plane_k<2>(b3, d, l3, u3);
+  // WA = [c0, c2, c1, c3], WB = [c4<<4, c6<<4, c5<<4, c7<<4] bytewise
   const uint32_t WA = (l1 & 0x01010101u) | (l2 & 0x02020202u) | (l3 & 0x04040404u);
   const uint32_t WB = (u1 & 0x10101010u) | (u2 & 0x20202020u) | (u3 & 0x40404040u);
-  const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), mad_hi(WA, d.k31, d.eb7x2), mad_lo(WB, d.k3, d.eb7x2),
-                         mad_hi(WB, d.k27, d.eb7x2)};
+  // (e_base + c) of elements (2j, 2j+1) on bits 7..14 / 23..30 of word j
+#if ZS_DEC_BAL
+  // (IMAD.HI with an addend needs a 64-bit addend register pair: the add goes to IADD3)
+  const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), mul_hi(WA, d.k31) + d.eb7x2, mad_lo(WB, d.k3, d.eb7x2),
+                         mul_hi(WB, d.k27) + d.eb7x2};
+#else
+  const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), (WA >> 1) + d.eb7x2, mad_lo(WB, d.k3, d.eb7x2),
+                         (WB >> 5) + d.eb7x2};
+#endif
   const uint32_t sel[4] = {ent.x, ent.y, ent.z, ent.w};
   uint32_t out[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const uint32_t P = prmt(hlo, hhi, sel[j]);
     const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);
-    out[j] = prmt(lpair, w, mad_hi(sel[j], d.k16, 0u));
+#if ZS_DEC_BAL == 1
+    out[j] = prmt(lpair, w, mul_hi(sel[j], d.k16));
+#elif ZS_DEC_BAL == 2
+    out[j] = prmt(lpair, w, j < 2 ? mul_hi(sel[j], d.k16) : (sel[j] >> 16));
+#else
+    out[j] = prmt(lpair, w, sel[j] >> 16);
+#endif
+  }
+  return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+// H window from two 8-B aligned shared loads (hbyte = shared address of the row's first H byte)
+__device__ __forceinline__ uint4 decode_row_v3h64(uint32_t b1, uint32_t b2, uint32_t b3, uint4 ent, uint32_t hbyte,
+                                                  uint32_t laddr, const DecConst& d) {
+  const uint2 q0 = ld_shared_v2(hbyte & ~7u), q1 = ld_shared_v2((hbyte & ~7u) + 8u);
+  const bool up = (hbyte & 4u) != 0u;
+  const uint32_t w0 = up ? q0.y : q0.x, w1 = up ? q1.x : q0.y, w2 = up ? q1.y : q1.x;
+  const uint32_t hlo = __funnelshift_r(w0, w1, hbyte * 8u);
+  const uint32_t hhi = __funnelshift_r(w1, w2, hbyte * 8u);
+#if ZS_DEC_BAL
+  const uint32_t lpair = mad_lo(ld_shared_u16(laddr + 2), d.k16, ld_shared_u16(laddr));
+#else
+  const uint32_t lpair = prmt(ld_shared_u16(laddr), ld_shared_u16(laddr + 2), 0x5410u);
+#endif
+  uint32_t l1, u1, l2, u2, l3, u3;
+  spread_plane_k<0>(b1, d, l1, u1);
+  spread_plane_k<1>(b2, d, l2, u2);
+  spread_plane_k<2>(b3, d, l3, u3);
+  // WA = [c0, c2, c1, c3], WB = [c4<<4, c6<<4, c5<<4, c7<<4] bytewise
+  const uint32_t WA = (l1 & 0x01010101u) | (l2 & 0x02020202u) | (l3 & 0x04040404u);
+  const uint32_t WB = (u1 & 0x10101010u) | (u2 & 0x20202020u) | (u3 & 0x40404040u);
+  // (e_base + c) of elements (2j, 2j+1) on bits 7..14 / 23..30 of word j
+#if ZS_DEC_BAL
+  // (IMAD.HI with an addend needs a 64-bit addend register pair: the add goes to IADD3)
+  const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), mul_hi(WA, d.k31) + d.eb7x2, mad_lo(WB, d.k3, d.eb7x2),
+                         mul_hi(WB, d.k27) + d.eb7x2};
+#else
+  const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), (WA >> 1) + d.eb7x2, mad_lo(WB, d.k3, d.eb7x2),
+                         (WB >> 5) + d.eb7x2};
+#endif
+  const uint32_t sel[4] = {ent.x, ent.y, ent.z, ent.w};
+  uint32_t out[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t P = prmt(hlo, hhi, sel[j]);
+    const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);
+#if ZS_DEC_BAL == 1
+    out[j] = prmt(lpair, w, mul_hi(sel[j], d.k16));
+#elif ZS_DEC_BAL == 2
+    out[j] = prmt(lpair, w, j < 2 ? mul_hi(sel[j], d.k16) : (sel[j] >> 16));
+#else
+    out[j] = prmt(lpair, w, sel[j] >> 16);
+#endif
   }
   return make_uint4(out[0], out[1], out[2], out[3]);
 }

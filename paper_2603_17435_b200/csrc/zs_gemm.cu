@@ -44,6 +44,15 @@ namespace zs {
 // The SMSP arbiter issues from the highest eligible warp id first, so the latency-critical
 // single-warp roles take the TOP ids (a low-id producer / MMA warp starves behind six busy
 // decoder warps on its SMSP and the whole pipeline idles): decoders 0..23, epilogue 24..27.
+#ifndef ZS_BACKOFF_CTRL
+#define ZS_BACKOFF_CTRL 256   // ns between barrier probes of the producer / MMA warps
+#endif
+#ifndef ZS_BACKOFF_DEC
+#define ZS_BACKOFF_DEC 32     // ns between barrier probes of a decoder warp
+#endif
+#ifndef ZS_H64
+#define ZS_H64 0   // 1: the row's H window from two 8-B loads (one wavefront per half-warp) + selects
+#endif
 #ifndef ZS_PRED_SEL
 #define ZS_PRED_SEL 0   // 1: skip the selector-table load for all-in-window rows (predicated LDS)
 #endif
@@ -59,10 +68,6 @@ constexpr int kWarpProdC = kWarpEpi0 + 6;
 constexpr int kWarpMma = kWarpEpi0 + 7;            // highest id: first pick of its SMSP's arbiter
 constexpr int kGemmThreads = 32 * (kWarpEpi0 + 8);  // 768 at D = 4 (80 registers per thread)
 constexpr int kUPS = 4;                            // units per ring stage
-#ifndef ZS_ROW_BATCH
-#define ZS_ROW_BATCH 4
-#endif
-constexpr int kRowBatch = ZS_ROW_BATCH;            // FragTile rows decoded together per thread
 constexpr int kMaxCSlots = 8;
 constexpr int kMaxXSlots = 16;
 constexpr int kMaxASlots = 12;
@@ -73,7 +78,8 @@ constexpr uint32_t kStageMeta = 128;               // see the stage header layou
 constexpr uint32_t kBtPlaneStride = 3 * kUPS * 512 + 32;
 constexpr uint32_t kStagePlanes = 2 * kBtPlaneStride;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kRpWarp = 32 * 16 + 32;          // per decoder warp: 32 FragTiles x 8 rows x u16 (+ pad)
+constexpr uint32_t kRpBuf = 32 * 16 + 64;           // row table: 32 FragTiles x 8 rows x u16 (+ pad)
+constexpr uint32_t kRpWarp = 2 * kRpBuf;             // per decoder warp: double-buffered (software pipeline)
 constexpr uint32_t kRpTabBytes = 4 * kDecPerQuarter * kRpWarp;
 
 // stage header (u32 words): [4i+0..3] unit i {H a, H b, L a, L b} offsets inside the
@@ -284,7 +290,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t nrun = (uint32_t)(rend - lane + 1);
       const int st_hi = min(nstages, (b0 + 32) / kUPS);
       for (int st = b0 / kUPS; st < st_hi; ++st, slot = (slot + 1 == S_c) ? 0u : slot + 1u, eph ^= (slot == 0)) {
-        mbar_wait(&bars->empty_c[slot], eph);
+        mbar_wait(&bars->empty_c[slot], eph, ZS_BACKOFF_CTRL);
         uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
         const bool mine = (quad == st - b0 / kUPS);
         // dbg & 8 (timing experiment): after the first ring fill the stages are not refilled;
@@ -338,7 +344,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t xr = 0, xuse = 0;   // X ring stage of st / how often the ring has wrapped
     grid_dependency_wait();      // X may be the previous kernel's output (PDL)
     for (int st = 0; st < nstages; ++st) {
-      if (xuse > 0) mbar_wait(&bars->xempty[xr], (xuse - 1u) & 1u);
+      if (xuse > 0) mbar_wait(&bars->xempty[xr], (xuse - 1u) & 1u, ZS_BACKOFF_CTRL);
       const int nu = min(kUPS, nunits - st * kUPS);
       if (elect_one()) {
         mbar_arrive_expect_tx(&bars->xfull[xr], xbytes * (uint32_t)nu);
@@ -382,9 +388,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t xa_end = xbase + S_x * p.aslot_bytes, ta_end = tmem_a + 32u * S_a;
     for (int st = 0; st < nstages; ++st) {
       const int i0 = st * kUPS, nu = min(kUPS, nunits - i0);
-      mbar_wait(&bars->xfull[xs], xph);
+      mbar_wait(&bars->xfull[xs], xph, ZS_BACKOFF_CTRL);
       try_signal();
-      mbar_wait(&bars->afull[as_], aph);          // all 4 x 4 unit-quarters of the stage decoded
+      mbar_wait(&bars->afull[as_], aph, ZS_BACKOFF_CTRL);   // all 4 x 4 unit-quarters of the stage decoded
       tc_fence_after();
       if (nu == kUPS && i0 != 0 && i0 + kUPS < nunits && kc != 0 && kc + kUPS < nbc) {
         // fast path: a full stage strictly inside one accumulation segment -> 16 MMAs from
@@ -471,45 +477,57 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;                       // TMEM lane quarter (== warp % 4)
     const int jd = (warp - kWarpDec0) >> 2;       // decoder index inside the quarter
     const int bt = q >> 1, hh = q & 1;
-    const int lr = lane + 32 * hh;                // row inside the BlockTile
-    const int fr = lr >> 3, r8 = lr & 7;
-    const int tr = fr >> 1;                       // TensorCoreTile row of this thread's FragTiles
-    const uint32_t obase = (uint32_t)(tr * 16 + (fr & 1));                 // o for fc = 0
     const uint32_t tq = tmem_a + ((uint32_t)(32 * q) << 16);
     const int fo = 32 * hh + lane;                // scan lane's FragTile
     uint8_t* rpt = rptab + (warp - kWarpDec0) * kRpWarp;
-    // row table: FragTile o (local 0..31) at o*16 + (o >> 4)*32 bytes, row r8 at + 2*r8 (the
-    // pad keeps the 4 FragTiles a warp reads at once on distinct banks)
-    const uint32_t rp_wr = (uint32_t)lane * 16u + ((uint32_t)lane >> 4) * 32u;
-    const uint32_t ol0 = obase - 32u * hh;        // local FragTile index for fc = 0
-    const uint32_t rb_off = ol0 * 16u + (ol0 >> 4) * 32u + 2u * (uint32_t)r8;
+    // Row passes (16x32bx2 TMEM stores): pass p covers rows 32 hh + 16 p + (lane & 15) of the
+    // BlockTile; lanes 0..15 decode FragTile columns 0..3 of those rows and lanes 16..31
+    // columns 4..7 of the SAME rows, so at every step the two half-warps read plane bytes
+    // 8 FragTiles (64 B) apart -- different banks -- instead of 16 FragTiles (128 B, the
+    // same banks) apart.
+    const int kh = lane >> 4;                     // column half: FragTile columns 4 kh .. 4 kh + 3
+    const int rl = lane & 15;
+    // row table: FragTile o (local 0..31) at o*16 + (o >> 3)*16 bytes, row r8 at + 2*r8 (the
+    // pad puts FragTiles o and o + 8 -- the two half-warps -- on different banks)
+    const uint32_t rp_wr = (uint32_t)lane * 16u + ((uint32_t)lane >> 3) * 16u;
     const uint32_t SAS = S_a / kUPS;
     DecConst dk;
     load_dec_const(dk, p.eb7x2);
     const uint32_t slut_b = smem_u32(slut);
     const uint32_t sbase = smem_u32(smem);
-    for (int u = jd; u < nunits; u += kDecPerQuarter) {
+    // Per-unit stage pointers (smem offsets) of unit u; waits for the unit's stage data.
+    struct UnitPtr {
+      uint32_t p1;     // BlockTile row's plane B1 slice of this unit (B2, B3 at + kUPS*512, 2*kUPS*512)
+      uint32_t hb;     // H segment base (16-B aligned)
+      uint32_t lb;     // L segment base
+      uint32_t slot;   // compressed ring slot
+    };
+    auto unit_ptr = [&](int u) {
       const uint32_t st = (uint32_t)u / kUPS, j = (uint32_t)u % kUPS;
       const uint32_t stc = fastdiv(st, S_c, p.cdiv_magic);
-      const uint32_t slot = st - stc * S_c, cph = stc & 1u;
-      const uint32_t ag = fastdiv(st, SAS, p.adiv_magic);  // use count of the A stage
-      const uint32_t astg = st - ag * SAS;                 // TMEM A stage of this unit
-      const uint32_t a = astg * kUPS + j;                  // TMEM A slot of this unit
+      const uint32_t slot = st - stc * S_c;
       const uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
       const uint32_t* meta = reinterpret_cast<const uint32_t*>(cs);
-      mbar_wait(&bars->full_c[slot], cph);
+      mbar_wait(&bars->full_c[slot], stc & 1u, ZS_BACKOFF_DEC);
       if (lane == 0) trace_ev(p.trace, u, 7 + q);
       // an absent BlockTile row b (odd row count) is aliased to row a: its rows decode valid
       // bytes into TMEM lanes whose outputs (rows >= N) the epilogue never stores
       const int btx = (bt == 1 && meta[20 + j] != 0u) ? 1 : 0;
       const uint4 mt = *reinterpret_cast<const uint4*>(meta + 4 * j);  // {H a, H b, L a, L b}
-      const uint8_t* P1 = cs + kStageMeta + btx * kBtPlaneStride + j * 512;
+      const uint8_t* Hr = cs + kStageMeta + kStagePlanes;
+      UnitPtr r;
+      r.p1 = (uint32_t)(cs + kStageMeta + btx * kBtPlaneStride + j * 512 - smem);
+      r.hb = (uint32_t)(Hr + btx * capH + (btx ? mt.y : mt.x) - smem);
+      r.lb = (uint32_t)(Hr + 2 * capH + btx * capL + (btx ? mt.w : mt.z) - smem);
+      r.slot = slot;
+      return r;
+    };
+    // Scan of unit u: lane = FragTile 32 hh + lane (canonical order); writes the H
+    // offset (from the BlockTile's H base) of each of its FragTile's 8 rows into row table buf.
+    auto scan_unit = [&](const UnitPtr& up, uint8_t* tab) {
+      const uint8_t* P1 = smem + up.p1;
       const uint8_t* P2 = P1 + kUPS * 512;
       const uint8_t* P3 = P2 + kUPS * 512;
-      const uint8_t* Hr = cs + kStageMeta + kStagePlanes;
-      const uint8_t* H = Hr + btx * capH + (btx ? mt.y : mt.x);
-      const uint8_t* L = Hr + 2 * capH + btx * capL + (btx ? mt.w : mt.z);
-      // ---- scan: lane = FragTile 32*hh + lane (canonical order)
       const uint2 s1 = *reinterpret_cast<const uint2*>(P1 + fo * 8);
       const uint2 s2 = *reinterpret_cast<const uint2*>(P2 + fo * 8);
       const uint2 s3 = *reinterpret_cast<const uint2*>(P3 + fo * 8);
@@ -528,36 +546,62 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint2 t3 = *reinterpret_cast<const uint2*>(P3 + lane * 8);
         excl += __reduce_add_sync(0xFFFFFFFFu, __popc(t1.x | t2.x | t3.x) + __popc(t1.y | t2.y | t3.y));
       }
-      // H byte offset (from this BlockTile's H base) of each of the FragTile's 8 rows, u16
       const uint32_t bl = bytepop(mlo), bh = bytepop(mhi);
       const uint32_t rp_lo = bl * 0x01010100u;
       const uint32_t rp_hi = bh * 0x01010100u + ((bl * 0x01010101u) >> 24) * 0x01010101u;
       const uint32_t ex2 = excl * 0x10001u;
-      const uint4 hrow = make_uint4(prmt(rp_lo, 0u, 0x4140u) + ex2, prmt(rp_lo, 0u, 0x4342u) + ex2,
-                                    prmt(rp_hi, 0u, 0x4140u) + ex2, prmt(rp_hi, 0u, 0x4342u) + ex2);
-      __syncwarp();   // previous unit's readers are done
-      *reinterpret_cast<uint4*>(rpt + rp_wr) = hrow;
-      __syncwarp();
+      *reinterpret_cast<uint4*>(tab + rp_wr) =
+          make_uint4(prmt(rp_lo, 0u, 0x4140u) + ex2, prmt(rp_lo, 0u, 0x4342u) + ex2, prmt(rp_hi, 0u, 0x4140u) + ex2,
+                     prmt(rp_hi, 0u, 0x4342u) + ex2);
+    };
+    // Software pipeline: the scan of the warp's NEXT unit runs between the two row passes of
+    // the current one, so its latency chain (loads -> popcounts -> 5 dependent shuffles ->
+    // table) overlaps row-decode work of the same warp instead of idling all four phase-aligned
+    // decoder warps of the SMSP at every stage boundary.
+    UnitPtr cur{};
+    if (jd < nunits) {
+      cur = unit_ptr(jd);
+      scan_unit(cur, rpt);
+    }
+    uint32_t tb = 0;                              // row table buffer of the current unit
+    for (int u = jd; u < nunits; u += kDecPerQuarter, tb ^= 1u) {
+      const int un = u + kDecPerQuarter;
+      const uint32_t st = (uint32_t)u / kUPS, j = (uint32_t)u % kUPS;
+      const uint32_t ag = fastdiv(st, SAS, p.adiv_magic);  // use count of the A stage
+      const uint32_t astg = st - ag * SAS;                 // TMEM A stage of this unit
+      const uint32_t a = astg * kUPS + j;                  // TMEM A slot of this unit
+      const uint8_t* tab = rpt + tb * kRpBuf;
+      __syncwarp();                                        // this unit's row table is written
       // the slot is free once the MMAs of stage st - SAS have completed (their commit)
       if (ag > 0) mbar_wait(&bars->afree[astg], (ag - 1u) & 1u);
       tc_fence_after();
+      if (lane == 0) trace_ev(p.trace, u, 11 + q);
+      UnitPtr nxt = cur;
       const uint32_t taddr0 = tq + 32u * a;
-      // per-row addresses = a per-unit base + an immediate.  FragTile of row f: o = obase +
-      // cf(f), cf(f) = (f>>1)*4 + (f&1)*2 (canonical order of FragTile column f).
-      const uint8_t* pb = P1 + obase * 8u + (uint32_t)r8;           // this row's plane byte, f = 0
-      const uint8_t* rb = rpt + rb_off;
-      const uint32_t hb = (uint32_t)(H - smem);                     // 16-B aligned
-      // fallback values of row f start at element 8*(o*8 + r8) - (its H offset) of the unit's L
-      const uint32_t la0 = (uint32_t)(L - smem) + 2u * hb + 16u * (obase * 8u + (uint32_t)r8);
-      uint32_t rare = 0;
+      const uint32_t hb = cur.hb;
 #pragma unroll
-      for (int fb = 0; fb < 8; fb += kRowBatch) {
-        if (p.dbg & 1) break;
-        uint4 v[kRowBatch];
+      for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) {                                          // next unit: wait for its data, scan
+          if (un < nunits) nxt = unit_ptr(un);
+          scan_unit(nxt, rpt + (tb ^ 1u) * kRpBuf);              // (the other table buffer)
+        }
+        if (p.dbg & 1) continue;
+        const int lr = 32 * hh + 16 * pass + rl;                    // row inside the BlockTile
+        const int fr = lr >> 3, r8 = lr & 7;
+        // FragTile of (row, column f): (lr >> 4) * 16 + cf(f) + (fr & 1), cf(f) = (f>>1)*4 + (f&1)*2;
+        // this lane's columns f = 4 kh + qq give cf = 8 kh + cf(qq)
+        const uint32_t ob = (uint32_t)((lr >> 4) * 16 + (fr & 1) + 8 * kh);   // FragTile for qq = 0
+        const uint32_t ol = ob - 32u * hh;                                    // local FragTile
+        const uint8_t* pb = smem + cur.p1 + ob * 8u + (uint32_t)r8;           // plane byte, qq = 0
+        const uint8_t* rb = tab + ol * 16u + (ol >> 3) * 16u + 2u * (uint32_t)r8;
+        // fallback values of the row start at element 8*(o*8 + r8) - (its H offset) of the L segment
+        const uint32_t la0 = cur.lb + 2u * hb + 16u * (ob * 8u + (uint32_t)r8);
+        uint4 v[4];
+        uint32_t rare = 0;
 #pragma unroll
-        for (int qq = 0; qq < kRowBatch; ++qq) {
-          const int f = fb + qq;
-          const uint32_t cf = (uint32_t)((f >> 1) * 4 + (f & 1) * 2);
+        for (int qq = 0; qq < 4; ++qq) {
+          const uint32_t cf = (uint32_t)((qq >> 1) * 4 + (qq & 1) * 2);
+          // table offset of FragTile ol + cf: cf in {0,2,4,6} never crosses an 8-FragTile pad
           const uint32_t hs_abs = hb + *reinterpret_cast<const uint16_t*>(rb + cf * 16u);
           const uint32_t b1 = pb[cf * 8u];
           const uint32_t b2 = pb[cf * 8u + kUPS * 512];
@@ -571,15 +615,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint4 ent = ld_shared_v4(slut_b + m * 16u);
 #endif
           rare |= ent.x;
+#if ZS_H64
+          v[qq] = decode_row_v3h64(b1, b2, b3, ent, sbase + hs_abs, sbase + la0 + 128u * cf - 2u * hs_abs, dk);
+#else
           v[qq] = decode_row_v3(b1, b2, b3, ent, sbase + (hs_abs & ~3u), hs_abs * 8u,
                                 sbase + la0 + 128u * cf - 2u * hs_abs, dk);
+#endif
         }
         if (__any_sync(0xFFFFFFFFu, rare & 0x80u)) {
-          // rare: a row of this batch has >= 3 fallbacks (rank >= 2); warp-uniform branch
+          // rare: a row of this pass has >= 3 fallbacks (rank >= 2); warp-uniform branch
 #pragma unroll
-          for (int qq = 0; qq < kRowBatch; ++qq) {
-            const int f = fb + qq;
-            const uint32_t cf = (uint32_t)((f >> 1) * 4 + (f & 1) * 2);
+          for (int qq = 0; qq < 4; ++qq) {
+            const uint32_t cf = (uint32_t)((qq >> 1) * 4 + (qq & 1) * 2);
             const uint32_t hs_abs = hb + *reinterpret_cast<const uint16_t*>(rb + cf * 16u);
             const uint32_t m = pb[cf * 8u] | pb[cf * 8u + kUPS * 512] | pb[cf * 8u + 2 * kUPS * 512];
             if (slut[m].x & 0x80u)
@@ -587,18 +634,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                           v[qq].y, v[qq].z, v[qq].w);
           }
         }
-        rare = 0;
         if (p.dbg & 2) {
           uint32_t x = 0;
 #pragma unroll
-          for (int qq = 0; qq < kRowBatch; ++qq) x ^= v[qq].x ^ v[qq].y ^ v[qq].z ^ v[qq].w;
+          for (int qq = 0; qq < 4; ++qq) x ^= v[qq].x ^ v[qq].y ^ v[qq].z ^ v[qq].w;
           if (x == 0x9E3779B9u) p.counters[0] = x;   // keeps the decode live
         } else {
-#if ZS_ROW_BATCH == 8
-          tmem_st32(taddr0, v);
-#else
-          tmem_st16(taddr0 + 4u * fb, v[0], v[1], v[2], v[3]);   // one 16-column store per 4 rows
-#endif
+          // TMEM lanes 32q + 16 pass + (0..15); half-warp kh writes columns 16 kh .. 16 kh + 15
+          tmem_st16x2(taddr0 + ((uint32_t)(16 * pass) << 16), v[0], v[1], v[2], v[3]);
         }
       }
       // publish the unit-quarter (release: the MMA warp's acquire on afull orders its MMAs
@@ -608,8 +651,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->afull[astg]);
       if (lane == 0) trace_ev(p.trace, u, 2 + q);
-      __syncwarp();                                    // all lanes done reading the stage
-      if (lane == 0) mbar_arrive(&bars->empty_c[slot]);
+      if (lane == 0) mbar_arrive(&bars->empty_c[cur.slot]);   // all lanes are done with the stage
+      cur = nxt;
     }
     // A partial last stage still needs its 16 afull arrivals: this warp's units past the end
     // that fall in that stage arrive without decoding (after the slot's previous use is

@@ -16,6 +16,9 @@ __device__ __forceinline__ uint32_t op(uint32_t a, uint32_t b, uint32_t c) {
   if (OP == 5) asm volatile("mad.lo.u32 %0, %1, 0x208041, %2;" : "=r"(d) : "r"(a), "r"(c));            // IMAD imm
   if (OP == 6) asm volatile("add.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(c));                         // IADD
   if (OP == 7) { float f; asm volatile("fma.rn.f32 %0, %1, %2, %3;" : "=f"(f) : "f"(__uint_as_float(a)), "f"(__uint_as_float(b)), "f"(__uint_as_float(c))); d = __float_as_uint(f); }
+  if (OP == 9) asm volatile("popc.b32 %0, %1;" : "=r"(d) : "r"(a));                                   // POPC
+  if (OP == 10) asm volatile("shfl.sync.up.b32 %0, %1, 1, 0, 0xffffffff;" : "=r"(d) : "r"(a));          // SHFL
+
   if (OP == 8) { d = a; asm volatile("{.reg .b32 t; mad.lo.u32 t, %1, %2, %3; lop3.b32 %0, t, %2, %3, 0xE4;}" : "=r"(d) : "r"(a), "r"(b), "r"(c)); }  // IMAD+LOP3 pair
   return d;
 }
@@ -73,5 +76,7 @@ int main() {
   run<6>("IADD", d, c);
   run<7>("FFMA", d, c);
   run<8>("IMAD+LOP3", d, c);
+  run<9>("POPC", d, c);
+  run<10>("SHFL", d, c);
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
 }

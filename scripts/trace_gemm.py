@@ -37,34 +37,26 @@ Z.gemm(x, wd)
 torch.cuda.synchronize()
 L.zs_debug_set_trace(None)
 t = tr.cpu().numpy().reshape(4, 128, 16).astype(np.int64)[:, :, :16]
-names = ["prod", "tick0", "dq0", "dq1", "dq2", "dq3", "mma", "dr0", "dr1", "dr2", "dr3", "as0", "as1", "as2", "as3", "tick1"]
-# summary over the first 4 CTAs: decode duration (slot-acquired -> done) and ticket->done
-d1, d2 = [], []
+names = ["prod", "-", "dq0", "dq1", "dq2", "dq3", "mma", "dr0", "dr1", "dr2", "dr3", "as0", "as1", "as2", "as3", "-"]
+# per unit-quarter (static assignment: decoder warp jd of quarter q takes units jd, jd+4, ...):
+#   dr = stage data ready (after the full-barrier wait), as = A slot free (scan + row table done,
+#   afree waited), dq = decoded and published
+scan, rows, gap = [], [], []
 for cta in range(4):
     for u in range(128):
         r = t[cta, u]
         for q in range(4):
-            if r[2 + q] and r[11 + q]:
-                d1.append(r[2 + q] - r[11 + q])
-            if r[2 + q] and r[7 + q]:
-                d2.append(r[2 + q] - r[7 + q])
-if d1:
-    print("decode (A slot ready -> done) cycles: mean %.0f  p10 %.0f  p90 %.0f" % (np.mean(d1), np.percentile(d1, 10), np.percentile(d1, 90)))
-if d2:
-    print("ticket -> done cycles: mean %.0f" % np.mean(d2))
-for cta in range(4):
-    r = t[cta]
-    nz = r[r > 0]
-    last_mma = r[:, 6].max()
-    first = nz.min()
-    n = int((r[:, 6] > 0).sum())
-    print(f"CTA {cta}: units traced {n}, span first->last MMA {last_mma - first} cycles, per unit {(last_mma - first) / max(n, 1):.0f}")
+            if r[7 + q] and r[11 + q] and r[2 + q]:
+                scan.append(r[11 + q] - r[7 + q])
+                rows.append(r[2 + q] - r[11 + q])
+            if u + 4 < 128 and r[2 + q] and t[cta, u + 4][7 + q]:
+                gap.append(t[cta, u + 4][7 + q] - r[2 + q])
+for name, d in (("scan+afree (dr->as)", scan), ("rows (as->dq)", rows), ("next unit wait (dq->dr')", gap)):
+    if d:
+        print("%-26s cycles: mean %6.0f  p10 %6.0f  p50 %6.0f  p90 %6.0f" % (name, np.mean(d), np.percentile(d, 10),
+                                                                            np.percentile(d, 50), np.percentile(d, 90)))
 for cta in range(1):
-    base = t[cta][t[cta] > 0].min()
-    print(f"CTA {cta}: times in cycles relative to first event")
-    print("unit " + " ".join(f"{n:>8s}" for n in names))
-    for u in range(0, 100):
-        row = t[cta, u]
-        if row.max() == 0:
-            break
-        print(f"{u:4d} " + " ".join(f"{(v - base) if v else -1:8d}" for v in row))
+    r = t[cta]
+    t0 = r[r > 0].min()
+    for u in range(0, 24):
+        print("u%3d " % u + " ".join("%s=%7d" % (names[e], r[u, e] - t0) for e in (0, 6, 7, 11, 2) if r[u, e]))

@@ -169,6 +169,27 @@ def test_gemm_full_size_gateup_sampled(zs, M):
     assert err <= TOL
 
 
+def test_gemm_full_size_gateup_integer_exact(zs):
+    # BASELINE config 2 at full size (224 bands x 64 K-steps over the bench's stream-K split)
+    # with integer weights {0, +-1..+-4} and activations {-4..4}: every fp32 partial sum is an
+    # exact integer, so Y must equal RNE_bf16 of the exact product bit for bit in any split-K
+    # order.  Checked: one column in every 128-row band (a different offset in each band),
+    # both band edges of every CTA boundary region, and two complete output rows.
+    K, N = G.LAYERS["L8B.GateUp"]
+    M = 32
+    w = G.integer_weights(N, K, seed=77)
+    x = G.integer_activations(M, K, seed=78)
+    y = to_np(zs.gemm(to_dev(x), zs.encode(w).to(DEV)))
+    bands = N // 128
+    cols = np.unique(np.concatenate([np.arange(bands) * 128 + (np.arange(bands) * 37) % 128,
+                                     np.arange(bands) * 128, np.arange(bands) * 128 + 127]))
+    exact = O.gemm_f64_cols(x, w, cols)
+    np.testing.assert_array_equal(y[:, cols], O.round_bf16_array(exact))
+    rows = [0, M - 1]
+    full = O.gemm_f64(x[rows], w)
+    np.testing.assert_array_equal(y[rows], O.round_bf16_array(full))
+
+
 def test_workspace_self_cleaning(zs):
     w = G.gaussian_bf16(1024, 4096, 0.02, 31)
     x = G.activations_bf16(24, 4096, 32)
