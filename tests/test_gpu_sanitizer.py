@@ -24,7 +24,7 @@ def test_sanitizer_clean(tool):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
-    cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "99", "--kernel-name", "regex:zipgemm|decompress",
+    cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "99", "--kernel-name", "regex=zipgemm|decompress",
            sys.executable, os.path.join(HERE, "sanitize_target.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
     out = r.stdout + r.stderr
