@@ -141,7 +141,7 @@ zs_status zs_decompress(const zs_tensor *w, uint16_t *out, int64_t ld_out, void 
  * At or below it the fused ZipGEMM kernel runs (decode stage).  Values measured on B200,
  * see DESIGN.md 7.3 (crossover of the two paths over LLaMA-3.1-8B layer shapes): matrices
  * of at most ZS_GEMM_SMALL_NK elements switch at ZS_GEMM_LARGE_M_SMALL_NK tokens. */
-#define ZS_GEMM_LARGE_M 128
+#define ZS_GEMM_LARGE_M 256
 #define ZS_GEMM_SMALL_NK (32ll * 1024 * 1024)
 #define ZS_GEMM_LARGE_M_SMALL_NK 48
 

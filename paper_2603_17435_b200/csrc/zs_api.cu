@@ -302,14 +302,32 @@ static zs_status gemm_core(const uint16_t* x, int64_t ldx, const zs_tensor* w, u
   // X tensor map: dims {K, M}, row stride ldx*2 bytes, box {64, n_umma}, SWIZZLE_128B;
   // out-of-bounds rows/columns are zero-filled by the TMA unit.
   const size_t budget = 227 * 1024;
-  // token chunk: the largest power of two <= 128 whose X slots plus a compressed ring of
-  // kGroups slots fit in shared memory (each chunk re-decodes W; see DESIGN.md large-M)
+  const size_t base = zs::gemm_fixed_smem();
+  // smem split for a token chunk of nu rows: X tiles (one per unit, [nu][64] bf16) and
+  // compressed stages (4 units each): at least 2 of each, so both streams stay double
+  // buffered; prefer up to 16 X tiles (L2-sourced, cheap) and then as many compressed stages
+  // as fit (the HBM stream is the one whose latency must be hidden)
+  auto split = [&](int64_t nu, uint32_t* nx, uint32_t* nc) {
+    const size_t xs = (size_t)up(nu * 128, 1024);
+    const size_t cs = p.cslot_bytes;
+    const uint32_t cmax = std::min<uint32_t>((uint32_t)zs::gemm_max_cslots(), g_max_cslots);
+    // preference: 3 compressed stages with >= 4 X tiles (measured best at small M; a 4th
+    // stage measured no change), then 2 stages with >= 4 tiles, then 2 with >= 2 tiles
+    static const uint32_t pref[][2] = {{3, 4}, {2, 4}, {2, 2}, {1, 2}};
+    for (const auto& pr : pref) {
+      const uint32_t c = std::min(pr[0], cmax);
+      if (base + c * cs + pr[1] * xs > budget) continue;
+      *nc = c;
+      *nx = (uint32_t)std::min<size_t>({(size_t)zs::gemm_max_xslots(), (size_t)8, (budget - base - c * cs) / xs});
+      return true;
+    }
+    return false;
+  };
+  // token chunk: the largest power of two <= 256 whose smem split fits (a chunk re-decodes W)
   int64_t chunk = zs::gemm_max_chunk();
   for (; chunk >= 16; chunk /= 2) {
-    const int64_t nu = up(std::min<int64_t>(chunk, M), 16);
-    const size_t xslot = (size_t)up(nu * 128, 1024);
-    const size_t fixed = zs::gemm_fixed_smem() + (size_t)zs::gemm_units_per_stage() * xslot;
-    if (fixed + (size_t)p.cslot_bytes <= budget) break;
+    uint32_t nx, nc;
+    if (split(up(std::min<int64_t>(chunk, M), 16), &nx, &nc)) break;
   }
   if (chunk < 16) return ZS_ERR_UNSUPPORTED;
   int launches = 0;
@@ -321,28 +339,18 @@ static zs_status gemm_core(const uint16_t* x, int64_t ldx, const zs_tensor* w, u
     p.mc = (int32_t)mc;
     p.n_umma = (uint32_t)up(mc, 16);
     p.aslot_bytes = (uint32_t)up((int64_t)p.n_umma * 128, 1024);
-    // smem split: compressed ring stages first (2..max, ~48 KB each at r = 0.98), X ring
-    // gets the rest (up to 16 tiles, at least 2)
-    const size_t base = zs::gemm_fixed_smem();
-    // X ring: 8 tiles normally; when that leaves room for fewer than 2 compressed stages
-    // (n_umma = 128: 16 KB tiles), one X stage (4 tiles) so the HBM stream stays double
-    // buffered -- the compressed fill latency is the one that must be hidden (8B GateUp
-    // M = 128: 132 -> 102 us, Down 80 -> 68 us)
-    size_t xmin = (size_t)std::max(8, 2 * zs::gemm_units_per_stage()) * p.aslot_bytes;
-    uint32_t nc = (uint32_t)std::min<size_t>(zs::gemm_max_cslots(), (budget - base - xmin) / p.cslot_bytes);
-    if (nc < 2) {
-      xmin = (size_t)zs::gemm_units_per_stage() * p.aslot_bytes;
-      nc = (uint32_t)std::min<size_t>(zs::gemm_max_cslots(), (budget - base - xmin) / p.cslot_bytes);
-    }
-    nc = std::min<uint32_t>(nc, g_max_cslots);
-    uint32_t nx = (uint32_t)std::min<size_t>(zs::gemm_max_xslots(), (budget - base - nc * (size_t)p.cslot_bytes) / p.aslot_bytes);
-    nx -= nx % (uint32_t)zs::gemm_units_per_stage();
-    if (nc < 1 || nx < (uint32_t)zs::gemm_units_per_stage()) return ZS_ERR_UNSUPPORTED;
+    uint32_t nx = 0, nc = 0;
+    if (!split(p.n_umma, &nx, &nc)) return ZS_ERR_UNSUPPORTED;
     p.n_cslots = nc;
     p.n_xslots = nx;
-    // TMEM: two accumulator buffers + an A-operand ring of 32-column slots (512 columns)
+    // TMEM (512 columns): accumulator buffer(s) + an A-operand ring of 32-column slots in
+    // whole stages of 4; two accumulator buffers when that leaves at least one A stage
     p.acc_cols = (uint32_t)up(p.n_umma, 32);
-    uint32_t na = (512u - 2u * p.acc_cols) / 32u;
+    // two buffers only while they leave a 2-stage A ring (8 slots): with a 1-stage ring the
+    // decoders and the MMA warp serialise per stage (measured: 8B GateUp M = 129, acc 160,
+    // 4 A slots: 123 us; one buffer + 8 slots is the better trade above 128 tokens)
+    p.n_acc = (2u * p.acc_cols + 2u * 32u * (uint32_t)zs::gemm_units_per_stage() <= 512u) ? 2u : 1u;
+    uint32_t na = (512u - p.n_acc * p.acc_cols) / 32u;
     na = std::min<uint32_t>(na, (uint32_t)zs::gemm_max_aslots());
     p.n_aslots = na - na % 4;
     auto magic = [](uint32_t d) { return d <= 1u ? 0u : (uint32_t)((1ull << 32) / d + 1ull); };

@@ -88,8 +88,8 @@ constexpr uint32_t kRpTabBytes = 4 * kDecPerQuarter * kRpWarp;
 struct __align__(16) Bars {
   uint64_t full_c[kMaxCSlots];
   uint64_t empty_c[kMaxCSlots];
-  uint64_t xfull[kMaxXSlots / kUPS];     // per X-ring stage (4 tiles)
-  uint64_t xempty[kMaxXSlots / kUPS];    // X stage consumed (tcgen05.commit after its last unit)
+  uint64_t xfull[kMaxXSlots];            // per X tile slot (one unit's [n_umma tokens][64 K])
+  uint64_t xempty[kMaxXSlots];           // X tile consumed (tcgen05.commit after its unit's MMAs)
   uint64_t afree[kMaxASlots / kUPS];    // TMEM A stage free (tcgen05.commit after its MMAs)
   uint64_t afull[kMaxASlots / kUPS];    // TMEM A stage decoded: one arrival per (unit, lane quarter)
   uint64_t accfull[2];
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&bars->full_c[i], 1);
       mbar_init(&bars->empty_c[i], 4 * kUPS);   // one arrival per (unit, lane quarter)
     }
-    for (uint32_t i = 0; i < S_x / kUPS; ++i) {
+    for (uint32_t i = 0; i < S_x; ++i) {
       mbar_init(&bars->xfull[i], 1);
       mbar_init(&bars->xempty[i], 1);
     }
@@ -234,7 +234,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 #endif
   const uint32_t dcols = p.acc_cols;                   // accumulator buffer stride (columns)
-  const uint32_t tmem_a = tmem_base + 2u * dcols;      // first A slot column
+  const uint32_t tmem_a = tmem_base + p.n_acc * dcols; // first A slot column
+  // accumulator buffer of segment s and the parity of its use (n_acc = 2: double buffered;
+  // n_acc = 1: a 256-token accumulator leaves room for one buffer next to the A ring)
+  const uint32_t nacc1 = p.n_acc - 1u;
+  auto abuf = [&](int s) { return (uint32_t)s & nacc1; };
+  auto apar = [&](int s) { return ((uint32_t)s >> nacc1) & 1u; };
 
   if (warp == kWarpProdC) {
     // ================================================================ compressed producer
@@ -336,29 +341,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == kWarpProdX) {
     // ================================================================ activation producer
-    // per stage: the 4 X tiles of its units land on one barrier; a stage slot is refilled
-    // once the MMA warp's commit after the slot's previous last unit has arrived
+    // one X tile [n_umma tokens][64 K] per unit into an S_x-slot ring; a slot is refilled once
+    // the MMA warp's commit after its unit's MMAs has arrived
     const uint64_t pol = policy_evict_last();
     const uint32_t xbytes = p.n_umma * 128u;
-    uint32_t kc = kc0;
-    uint32_t xr = 0, xuse = 0;   // X ring stage of st / how often the ring has wrapped
+    uint32_t k = kc0;
+    uint32_t xs = 0, xuse = 0;   // tile slot / how often the ring has wrapped
     grid_dependency_wait();      // X may be the previous kernel's output (PDL)
-    for (int st = 0; st < nstages; ++st) {
-      if (xuse > 0) mbar_wait(&bars->xempty[xr], (xuse - 1u) & 1u, ZS_BACKOFF_CTRL);
-      const int nu = min(kUPS, nunits - st * kUPS);
+    for (int it = 0; it < nunits; ++it) {
+      if (xuse > 0) mbar_wait(&bars->xempty[xs], (xuse - 1u) & 1u, ZS_BACKOFF_CTRL);
       if (elect_one()) {
-        mbar_arrive_expect_tx(&bars->xfull[xr], xbytes * (uint32_t)nu);
-        uint32_t k = kc;
-        for (int i = 0; i < nu; ++i) {
-          tma_load_2d(xslots + (size_t)(xr * kUPS + i) * p.aslot_bytes, &xmap, (int32_t)(k * 64), p.m0,
-                      &bars->xfull[xr], pol);
-          if (++k == nbc) k = 0;
-        }
+        mbar_arrive_expect_tx(&bars->xfull[xs], xbytes);
+        tma_load_2d(xslots + (size_t)xs * p.aslot_bytes, &xmap, (int32_t)(k * 64), p.m0, &bars->xfull[xs], pol);
       }
       __syncwarp();
-      kc += (uint32_t)nu;
-      if (kc >= nbc) kc -= nbc;
-      if (++xr == SXS) { xr = 0; ++xuse; }
+      if (++k == nbc) k = 0;
+      if (++xs == S_x) { xs = 0; ++xuse; }
     }
   } else if (warp == kWarpMma) {
     // ================================================================ MMA issuer
@@ -370,6 +368,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t idesc = umma_idesc_bf16(128, p.n_umma);
     const uint32_t xbase = smem_u32(xslots);
     const uint32_t SAS = S_a / kUPS;
+    const uint32_t nacc = p.n_acc;
     uint32_t kc = kc0;
     int seg = -1;
     // Accumulator hand-off to the epilogue on hardware named barriers 2/3 (sleeping warps
@@ -377,42 +376,71 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int sig = 0;                                                // segments signalled
     // segments < seg are fully issued: wake the epilogue for those whose accumulator is done
     auto try_signal = [&]() {
-      while (sig < seg && mbar_test_wait(&bars->accfull[sig & 1], ((uint32_t)sig >> 1) & 1u)) {
+      while (sig < seg && mbar_test_wait(&bars->accfull[abuf(sig)], apar(sig))) {
         named_bar_arrive(2 + (sig & 1), 160);
         ++sig;
       }
     };
-    uint32_t xs = 0, xph = 0;                     // X stage ring slot / parity
+    uint32_t xs = 0, xph = 0;                     // X tile slot / parity of its fill
     uint32_t as_ = 0, aph = 0;                    // A stage ring slot / parity of its afull phase
-    uint32_t xa = xbase, ta = tmem_a;             // X tile address / A slot column of the stage
-    const uint32_t xa_end = xbase + S_x * p.aslot_bytes, ta_end = tmem_a + 32u * S_a;
+    uint32_t ta = tmem_a;                         // A slot column of the stage
+    const uint32_t ta_end = tmem_a + 32u * S_a;
     for (int st = 0; st < nstages; ++st) {
       const int i0 = st * kUPS, nu = min(kUPS, nunits - i0);
-      mbar_wait(&bars->xfull[xs], xph, ZS_BACKOFF_CTRL);
+      // the stage's X tiles: slots xs, xs + 1, ... (mod S_x)
+      uint32_t xsl[kUPS], xpl[kUPS];
+#pragma unroll
+      for (int j = 0; j < kUPS; ++j) {
+        xsl[j] = xs;
+        xpl[j] = xph;
+        if (j < nu && ++xs == S_x) { xs = 0; xph ^= 1u; }
+      }
       try_signal();
       mbar_wait(&bars->afull[as_], aph, ZS_BACKOFF_CTRL);   // all 4 x 4 unit-quarters of the stage decoded
       tc_fence_after();
       if (nu == kUPS && i0 != 0 && i0 + kUPS < nunits && kc != 0 && kc + kUPS < nbc) {
-        // fast path: a full stage strictly inside one accumulation segment -> 16 MMAs from
-        // one set of per-stage operands (the stage's A slots and X tiles are contiguous)
-        const uint32_t d = tmem_base + (uint32_t)(seg & 1) * dcols;
-        const uint64_t bdesc = umma_desc_sw128(xa);
-        const uint32_t bstep = p.aslot_bytes >> 4;   // descriptor address units per X tile
-        if (elect_one()) {
-          if (!(p.dbg & 4)) {
+        // fast path: a full stage strictly inside one accumulation segment -> 16 MMAs
+        const uint32_t d = tmem_base + abuf(seg) * dcols;
+        if (S_x >= (uint32_t)kUPS) {
+          // the stage's 4 tiles are all in the ring: one wait set, 16 back-to-back MMAs
 #pragma unroll
-            for (int i = 0; i < kUPS; ++i) {
-              const uint64_t bd = bdesc + (uint64_t)(bstep * (uint32_t)i);
+          for (int i = 0; i < kUPS; ++i) mbar_wait(&bars->xfull[xsl[i]], xpl[i], ZS_BACKOFF_CTRL);
+          tc_fence_after();
+          if (elect_one()) {
+            if (!(p.dbg & 4)) {
+#pragma unroll
+              for (int i = 0; i < kUPS; ++i) {
+                const uint64_t bd = umma_desc_sw128(xbase + xsl[i] * p.aslot_bytes);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) umma_bf16_ts(d, ta + 32u * i + 8u * k, bd + 2 * k, idesc, 1u);
+              }
+            }
+            umma_commit(&bars->afree[as_]);
+#pragma unroll
+            for (int i = 0; i < kUPS; ++i) umma_commit(&bars->xempty[xsl[i]]);
+          }
+          __syncwarp();
+        } else {
+        // each unit's X tile is awaited right before its MMAs and released right after them:
+        // the tile ring holds fewer tiles than a stage has units (256-token chunks)
+#pragma unroll
+        for (int i = 0; i < kUPS; ++i) {
+          mbar_wait(&bars->xfull[xsl[i]], xpl[i], ZS_BACKOFF_CTRL);
+          tc_fence_after();
+          if (elect_one()) {
+            if (!(p.dbg & 4)) {
+              const uint64_t bd = umma_desc_sw128(xbase + xsl[i] * p.aslot_bytes);
 #pragma unroll
               for (int k = 0; k < 4; ++k) umma_bf16_ts(d, ta + 32u * i + 8u * k, bd + 2 * k, idesc, 1u);
             }
+            umma_commit(&bars->xempty[xsl[i]]);
           }
-          umma_commit(&bars->afree[as_]);
-          umma_commit(&bars->xempty[xs]);
+          __syncwarp();
         }
+        if (elect_one()) umma_commit(&bars->afree[as_]);
         __syncwarp();
+        }
         ta += 32u * kUPS; if (ta == ta_end) ta = tmem_a;
-        xa += kUPS * p.aslot_bytes; if (xa == xa_end) xa = xbase;
         kc += kUPS;
       } else {
         for (int j = 0; j < nu; ++j) {
@@ -421,17 +449,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const bool last = (it == nunits - 1) || (kc + 1 == nbc);
           if (first) {
             ++seg;
-            // the epilogue must have been woken for segment seg - 2 before its buffer is reused
-            while (sig + 1 < seg) {
-              mbar_wait(&bars->accfull[sig & 1], ((uint32_t)sig >> 1) & 1u);
+            // the epilogue must have been woken for segment seg - n_acc (the previous user of
+            // this accumulator buffer) before the buffer is reused
+            while (sig + (int)nacc <= seg) {
+              mbar_wait(&bars->accfull[abuf(sig)], apar(sig));
               named_bar_arrive(2 + (sig & 1), 160);
               ++sig;
             }
-            mbar_wait(&bars->accempty[seg & 1], (((uint32_t)seg >> 1) & 1u) ^ 1u);
+            mbar_wait(&bars->accempty[abuf(seg)], apar(seg) ^ 1u);
             tc_fence_after();
           }
-          const uint32_t d = tmem_base + (uint32_t)(seg & 1) * dcols;
-          const uint64_t bdesc = umma_desc_sw128(xa);
+          const uint32_t d = tmem_base + abuf(seg) * dcols;
+          const uint64_t bdesc = umma_desc_sw128(xbase + xsl[j] * p.aslot_bytes);
+          mbar_wait(&bars->xfull[xsl[j]], xpl[j], ZS_BACKOFF_CTRL);
+          tc_fence_after();
           if (elect_one()) {
             if (!(p.dbg & 4)) {
 #pragma unroll
@@ -439,15 +470,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 umma_bf16_ts(d, ta + 8u * k, bdesc + 2 * k, idesc, (first && k == 0) ? 0u : 1u);
             }
             trace_ev(p.trace, it, 6);
-            if (last) umma_commit(&bars->accfull[seg & 1]);
-            if (j == nu - 1) {
-              umma_commit(&bars->afree[as_]);
-              umma_commit(&bars->xempty[xs]);
-            }
+            if (last) umma_commit(&bars->accfull[abuf(seg)]);
+            umma_commit(&bars->xempty[xsl[j]]);
+            if (j == nu - 1) umma_commit(&bars->afree[as_]);
           }
           __syncwarp();
           ta += 32u; if (ta == ta_end) ta = tmem_a;
-          xa += p.aslot_bytes; if (xa == xa_end) xa = xbase;
           if (++kc == nbc) kc = 0;
         }
         // a partial last stage leaves its remaining A slots unused: skip them
@@ -456,11 +484,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       if (++as_ == SAS) { as_ = 0; aph ^= 1u; }
-      if (++xs == SXS) { xs = 0; xph ^= 1u; }
     }
     // the last segment(s): wait for their accumulators, then wake the epilogue
     while (sig <= seg) {
-      mbar_wait(&bars->accfull[sig & 1], ((uint32_t)sig >> 1) & 1u);
+      mbar_wait(&bars->accfull[abuf(sig)], apar(sig));
       named_bar_arrive(2 + (sig & 1), 160);
       ++sig;
     }
@@ -678,11 +705,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // complete; the mbarrier wait after it then passes at once (and orders the TMEM reads)
       named_bar_sync(2 + (seg & 1), 160);
       if (seg == 0) grid_dependency_wait();   // Y / workspace / counters: previous kernel done (PDL)
-      mbar_wait(&bars->accfull[seg & 1], ((uint32_t)seg >> 1) & 1u);
+      mbar_wait(&bars->accfull[abuf(seg)], apar(seg));
       tc_fence_after();
       const int64_t n = (int64_t)band * 128 + et;
       const bool nvalid = n < p.N;
-      const uint32_t taddr = tmem_base + ((uint32_t)(32 * eq) << 16) + (uint32_t)(seg & 1) * dcols;
+      const uint32_t taddr = tmem_base + ((uint32_t)(32 * eq) << 16) + abuf(seg) * dcols;
       for (uint32_t cb = 0; cb < p.n_umma; cb += 16) {
         uint32_t v[16];
         tmem_ld16(taddr + cb, v);
@@ -704,7 +731,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&bars->accempty[seg & 1]);
+      mbar_arrive(&bars->accempty[abuf(seg)]);
       if (kPeer && full && nvalid && p.npeer > 0)
         copy_to_peers(p.ypeer, p.npeer, p.y, p.ldy, (int64_t)p.m0 * p.ldy + n, p.mc);
       if (!full) {
@@ -794,7 +821,7 @@ int gemm_max_cslots() { return kMaxCSlots; }
 int gemm_max_aslots() { return kMaxASlots; }
 uint32_t gemm_stage_fixed_bytes() { return kStageMeta + kStagePlanes; }
 int gemm_units_per_stage() { return kUPS; }
-int gemm_max_chunk() { return 128; }
+int gemm_max_chunk() { return 256; }
 uint32_t gemm_fixed_smem() { return 1024 + 1024 + kRpTabBytes + 4096; }
 
 }  // namespace zs

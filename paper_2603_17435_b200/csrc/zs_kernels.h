@@ -66,9 +66,10 @@ struct GemmParams {
   uint32_t cslot_bytes;     // compressed ring stage (4 units)
   uint32_t aslot_bytes;     // X (B operand) slot; the decoded A operand lives in TMEM
   uint32_t n_cslots;        // ring stages
-  uint32_t n_xslots;        // X tile ring
+  uint32_t n_xslots;        // X tile ring (one tile = one unit's [n_umma][64] X slice)
   uint32_t n_aslots;        // TMEM A-operand ring (32 columns each, multiple of 4)
   uint32_t acc_cols;        // TMEM columns per accumulator buffer (>= n_umma, multiple of 32)
+  uint32_t n_acc;           // accumulator buffers: 2 (double buffered), 1 when 2 x acc_cols leaves no A ring
   uint32_t eb7x2;
   uint32_t cdiv_magic, adiv_magic;  // fastdiv multipliers of n_cslots / n_aslots
   unsigned long long* trace;  // optional per-unit event timestamps (debug; nullptr = off)
