@@ -188,6 +188,10 @@ extern "C" zs_status zs_decompress(const zs_tensor* w, uint16_t* out, int64_t ld
   return ZS_OK;
 }
 
+#ifndef ZS_XTILES_MAX
+#define ZS_XTILES_MAX 12   // X tiles in the ring at most (L2-sourced; 3 stages of 4 units)
+#endif
+
 // split-K region: fp32 partials [min(M,256)][N] + per-band counters (zero between calls)
 static size_t splitk_bytes(int64_t M, int64_t N) {
   const int64_t mc = up(std::min<int64_t>(M, 256), 16);   // row stride of the [N][mc] partials
@@ -318,7 +322,7 @@ static zs_status gemm_core(const uint16_t* x, int64_t ldx, const zs_tensor* w, u
       const uint32_t c = std::min(pr[0], cmax);
       if (base + c * cs + pr[1] * xs > budget) continue;
       *nc = c;
-      *nx = (uint32_t)std::min<size_t>({(size_t)zs::gemm_max_xslots(), (size_t)8, (budget - base - c * cs) / xs});
+      *nx = (uint32_t)std::min<size_t>({(size_t)zs::gemm_max_xslots(), (size_t)ZS_XTILES_MAX, (budget - base - c * cs) / xs});
       return true;
     }
     return false;

@@ -348,15 +348,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t k = kc0;
     uint32_t xs = 0, xuse = 0;   // tile slot / how often the ring has wrapped
     grid_dependency_wait();      // X may be the previous kernel's output (PDL)
-    for (int it = 0; it < nunits; ++it) {
-      if (xuse > 0) mbar_wait(&bars->xempty[xs], (xuse - 1u) & 1u, ZS_BACKOFF_CTRL);
+    // groups of g tiles per wait/issue round: a stage's 4 tiles when the ring holds them
+    // (fewer control-warp instructions on a decoder SMSP), else one tile at a time
+    const int g = (S_x >= (uint32_t)kUPS) ? kUPS : 1;
+    for (int it0 = 0; it0 < nunits; it0 += g) {
+      const int ng = min(g, nunits - it0);
+      uint32_t s = xs, u = xuse;
+      for (int i = 0; i < ng; ++i) {
+        if (u > 0) mbar_wait(&bars->xempty[s], (u - 1u) & 1u, ZS_BACKOFF_CTRL);
+        if (++s == S_x) { s = 0; ++u; }
+      }
       if (elect_one()) {
-        mbar_arrive_expect_tx(&bars->xfull[xs], xbytes);
-        tma_load_2d(xslots + (size_t)xs * p.aslot_bytes, &xmap, (int32_t)(k * 64), p.m0, &bars->xfull[xs], pol);
+        uint32_t s2 = xs, k2 = k;
+        for (int i = 0; i < ng; ++i) {
+          mbar_arrive_expect_tx(&bars->xfull[s2], xbytes);
+          tma_load_2d(xslots + (size_t)s2 * p.aslot_bytes, &xmap, (int32_t)(k2 * 64), p.m0, &bars->xfull[s2], pol);
+          if (++s2 == S_x) s2 = 0;
+          if (++k2 == nbc) k2 = 0;
+        }
       }
       __syncwarp();
-      if (++k == nbc) k = 0;
-      if (++xs == S_x) { xs = 0; ++xuse; }
+      xs = s;
+      xuse = u;
+      for (int i = 0; i < ng; ++i)
+        if (++k == nbc) k = 0;
     }
   } else if (warp == kWarpMma) {
     // ================================================================ MMA issuer
