@@ -193,23 +193,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t band0 = u0 / nbc, kc0 = u0 % nbc;
 
   // ---- setup
-  if (tid < 256) slut[tid] = __ldg(&c_lut[tid]);
-  if (tid == 32) {
-    for (uint32_t i = 0; i < S_c; ++i) {
+  // barrier init spread over the lanes of warp 1 (the selector table is loaded by the decoder
+  // warps after the CTA barrier, off the producers' critical path)
+  if (warp == 1) {
+    for (uint32_t i = lane; i < S_c; i += 32) {
       mbar_init(&bars->full_c[i], 1);
       mbar_init(&bars->empty_c[i], 4 * kUPS);   // one arrival per (unit, lane quarter)
     }
-    for (uint32_t i = 0; i < S_x; ++i) {
+    for (uint32_t i = lane; i < S_x; i += 32) {
       mbar_init(&bars->xfull[i], 1);
       mbar_init(&bars->xempty[i], 1);
     }
-    for (uint32_t i = 0; i < S_a / kUPS; ++i) {
-      mbar_init(&bars->afree[i], 1);
-      mbar_init(&bars->afull[i], 4 * kUPS);
+    if (lane < S_a / kUPS) {
+      mbar_init(&bars->afree[lane], 1);
+      mbar_init(&bars->afull[lane], 4 * kUPS);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars->accfull[i], 1);
-      mbar_init(&bars->accempty[i], 128);
+    if (lane < 2) {
+      mbar_init(&bars->accfull[lane], 1);
+      mbar_init(&bars->accempty[lane], 128);
     }
     fence_mbar_init();
   }
@@ -238,6 +239,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // accumulator buffer of segment s and the parity of its use (n_acc = 2: double buffered;
   // n_acc = 1: a 256-token accumulator leaves room for one buffer next to the A ring)
   const uint32_t nacc1 = p.n_acc - 1u;
+  // X ring in stage mode (>= 2 stages of 4 tiles: one barrier per stage, contiguous tiles) or
+  // tile mode (one barrier per tile; the 256-token chunks' 32-KB tiles)
+  const bool xstage = (S_x % kUPS) == 0 && S_x >= 2 * kUPS;
   auto abuf = [&](int s) { return (uint32_t)s & nacc1; };
   auto apar = [&](int s) { return ((uint32_t)s >> nacc1) & 1u; };
 
@@ -348,30 +352,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t k = kc0;
     uint32_t xs = 0, xuse = 0;   // tile slot / how often the ring has wrapped
     grid_dependency_wait();      // X may be the previous kernel's output (PDL)
-    // groups of g tiles per wait/issue round: a stage's 4 tiles when the ring holds them
-    // (fewer control-warp instructions on a decoder SMSP), else one tile at a time
-    const int g = (S_x >= (uint32_t)kUPS) ? kUPS : 1;
-    for (int it0 = 0; it0 < nunits; it0 += g) {
-      const int ng = min(g, nunits - it0);
-      uint32_t s = xs, u = xuse;
-      for (int i = 0; i < ng; ++i) {
-        if (u > 0) mbar_wait(&bars->xempty[s], (u - 1u) & 1u, ZS_BACKOFF_CTRL);
-        if (++s == S_x) { s = 0; ++u; }
-      }
-      if (elect_one()) {
-        uint32_t s2 = xs, k2 = k;
-        for (int i = 0; i < ng; ++i) {
-          mbar_arrive_expect_tx(&bars->xfull[s2], xbytes);
-          tma_load_2d(xslots + (size_t)s2 * p.aslot_bytes, &xmap, (int32_t)(k2 * 64), p.m0, &bars->xfull[s2], pol);
-          if (++s2 == S_x) s2 = 0;
-          if (++k2 == nbc) k2 = 0;
+    if (xstage) {
+      // stage mode (the ring holds >= 2 stages of 4 tiles): one barrier per stage of 4 tiles
+      uint32_t xr = 0;
+      for (int st = 0; st < nstages; ++st) {
+        if (xuse > 0) mbar_wait(&bars->xempty[xr], (xuse - 1u) & 1u, ZS_BACKOFF_CTRL);
+        const int nu = min(kUPS, nunits - st * kUPS);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&bars->xfull[xr], xbytes * (uint32_t)nu);
+          uint32_t k2 = k;
+          for (int i = 0; i < nu; ++i) {
+            tma_load_2d(xslots + (size_t)(xr * kUPS + i) * p.aslot_bytes, &xmap, (int32_t)(k2 * 64), p.m0,
+                        &bars->xfull[xr], pol);
+            if (++k2 == nbc) k2 = 0;
+          }
         }
+        __syncwarp();
+        k += (uint32_t)nu;
+        if (k >= nbc) k -= nbc;
+        if (++xr == S_x / kUPS) { xr = 0; ++xuse; }
       }
-      __syncwarp();
-      xs = s;
-      xuse = u;
-      for (int i = 0; i < ng; ++i)
+    } else {
+      // tile mode (256-token chunks: fewer tiles than 2 stages fit): one barrier per tile
+      for (int it = 0; it < nunits; ++it) {
+        if (xuse > 0) mbar_wait(&bars->xempty[xs], (xuse - 1u) & 1u, ZS_BACKOFF_CTRL);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&bars->xfull[xs], xbytes);
+          tma_load_2d(xslots + (size_t)xs * p.aslot_bytes, &xmap, (int32_t)(k * 64), p.m0, &bars->xfull[xs], pol);
+        }
+        __syncwarp();
         if (++k == nbc) k = 0;
+        if (++xs == S_x) { xs = 0; ++xuse; }
+      }
     }
   } else if (warp == kWarpMma) {
     // ================================================================ MMA issuer
@@ -396,19 +408,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         ++sig;
       }
     };
-    uint32_t xs = 0, xph = 0;                     // X tile slot / parity of its fill
+    uint32_t xs = 0, xph = 0;                     // X slot (stage mode: stage slot) / parity of its fill
     uint32_t as_ = 0, aph = 0;                    // A stage ring slot / parity of its afull phase
     uint32_t ta = tmem_a;                         // A slot column of the stage
     const uint32_t ta_end = tmem_a + 32u * S_a;
+    const uint32_t SXS = S_x / kUPS;
     for (int st = 0; st < nstages; ++st) {
       const int i0 = st * kUPS, nu = min(kUPS, nunits - i0);
-      // the stage's X tiles: slots xs, xs + 1, ... (mod S_x)
+      // X tile of unit j of the stage: slot / fill parity (tile mode), or the stage's slot
       uint32_t xsl[kUPS], xpl[kUPS];
+      if (xstage) {
 #pragma unroll
-      for (int j = 0; j < kUPS; ++j) {
-        xsl[j] = xs;
-        xpl[j] = xph;
-        if (j < nu && ++xs == S_x) { xs = 0; xph ^= 1u; }
+        for (int j = 0; j < kUPS; ++j) { xsl[j] = xs * kUPS + (uint32_t)j; xpl[j] = xph; }
+        mbar_wait(&bars->xfull[xs], xph, ZS_BACKOFF_CTRL);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kUPS; ++j) {
+          xsl[j] = xs;
+          xpl[j] = xph;
+          if (j < nu && ++xs == S_x) { xs = 0; xph ^= 1u; }
+        }
       }
       try_signal();
       mbar_wait(&bars->afull[as_], aph, ZS_BACKOFF_CTRL);   // all 4 x 4 unit-quarters of the stage decoded
@@ -416,44 +435,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (nu == kUPS && i0 != 0 && i0 + kUPS < nunits && kc != 0 && kc + kUPS < nbc) {
         // fast path: a full stage strictly inside one accumulation segment -> 16 MMAs
         const uint32_t d = tmem_base + abuf(seg) * dcols;
-        if (S_x >= (uint32_t)kUPS) {
-          // the stage's 4 tiles are all in the ring: one wait set, 16 back-to-back MMAs
-#pragma unroll
-          for (int i = 0; i < kUPS; ++i) mbar_wait(&bars->xfull[xsl[i]], xpl[i], ZS_BACKOFF_CTRL);
-          tc_fence_after();
+        if (xstage) {
+          // the stage's 4 tiles are contiguous: one descriptor base, 16 back-to-back MMAs
+          const uint64_t bdesc = umma_desc_sw128(xbase + xsl[0] * p.aslot_bytes);
+          const uint32_t bstep = p.aslot_bytes >> 4;   // descriptor address units per X tile
           if (elect_one()) {
             if (!(p.dbg & 4)) {
 #pragma unroll
               for (int i = 0; i < kUPS; ++i) {
-                const uint64_t bd = umma_desc_sw128(xbase + xsl[i] * p.aslot_bytes);
+                const uint64_t bd = bdesc + (uint64_t)(bstep * (uint32_t)i);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) umma_bf16_ts(d, ta + 32u * i + 8u * k, bd + 2 * k, idesc, 1u);
               }
             }
             umma_commit(&bars->afree[as_]);
-#pragma unroll
-            for (int i = 0; i < kUPS; ++i) umma_commit(&bars->xempty[xsl[i]]);
+            umma_commit(&bars->xempty[xs]);
           }
           __syncwarp();
         } else {
-        // each unit's X tile is awaited right before its MMAs and released right after them:
-        // the tile ring holds fewer tiles than a stage has units (256-token chunks)
+          // each unit's tile is awaited right before its MMAs and released right after them
 #pragma unroll
-        for (int i = 0; i < kUPS; ++i) {
-          mbar_wait(&bars->xfull[xsl[i]], xpl[i], ZS_BACKOFF_CTRL);
-          tc_fence_after();
-          if (elect_one()) {
-            if (!(p.dbg & 4)) {
-              const uint64_t bd = umma_desc_sw128(xbase + xsl[i] * p.aslot_bytes);
+          for (int i = 0; i < kUPS; ++i) {
+            mbar_wait(&bars->xfull[xsl[i]], xpl[i], ZS_BACKOFF_CTRL);
+            tc_fence_after();
+            if (elect_one()) {
+              if (!(p.dbg & 4)) {
+                const uint64_t bd = umma_desc_sw128(xbase + xsl[i] * p.aslot_bytes);
 #pragma unroll
-              for (int k = 0; k < 4; ++k) umma_bf16_ts(d, ta + 32u * i + 8u * k, bd + 2 * k, idesc, 1u);
+                for (int k = 0; k < 4; ++k) umma_bf16_ts(d, ta + 32u * i + 8u * k, bd + 2 * k, idesc, 1u);
+              }
+              umma_commit(&bars->xempty[xsl[i]]);
             }
-            umma_commit(&bars->xempty[xsl[i]]);
+            __syncwarp();
           }
+          if (elect_one()) umma_commit(&bars->afree[as_]);
           __syncwarp();
-        }
-        if (elect_one()) umma_commit(&bars->afree[as_]);
-        __syncwarp();
         }
         ta += 32u * kUPS; if (ta == ta_end) ta = tmem_a;
         kc += kUPS;
@@ -476,8 +492,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           const uint32_t d = tmem_base + abuf(seg) * dcols;
           const uint64_t bdesc = umma_desc_sw128(xbase + xsl[j] * p.aslot_bytes);
-          mbar_wait(&bars->xfull[xsl[j]], xpl[j], ZS_BACKOFF_CTRL);
-          tc_fence_after();
+          if (!xstage) {
+            mbar_wait(&bars->xfull[xsl[j]], xpl[j], ZS_BACKOFF_CTRL);
+            tc_fence_after();
+          }
           if (elect_one()) {
             if (!(p.dbg & 4)) {
 #pragma unroll
@@ -486,8 +504,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
             trace_ev(p.trace, it, 6);
             if (last) umma_commit(&bars->accfull[abuf(seg)]);
-            umma_commit(&bars->xempty[xsl[j]]);
-            if (j == nu - 1) umma_commit(&bars->afree[as_]);
+            if (!xstage) umma_commit(&bars->xempty[xsl[j]]);
+            if (j == nu - 1) {
+              umma_commit(&bars->afree[as_]);
+              if (xstage) umma_commit(&bars->xempty[xs]);
+            }
           }
           __syncwarp();
           ta += 32u; if (ta == ta_end) ta = tmem_a;
@@ -498,6 +519,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           ta += 32u * (uint32_t)(kUPS - nu); if (ta >= ta_end) ta -= ta_end - tmem_a;
         }
       }
+      if (xstage && ++xs == SXS) { xs = 0; xph ^= 1u; }
       if (++as_ == SAS) { as_ = 0; aph ^= 1u; }
     }
     // the last segment(s): wait for their accumulators, then wake the epilogue
@@ -537,6 +559,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     load_dec_const(dk, p.eb7x2);
     const uint32_t slut_b = smem_u32(slut);
     const uint32_t sbase = smem_u32(smem);
+    if (tid < 256) slut[tid] = __ldg(&c_lut[tid]);
+    named_bar_sync(4, 32 * 4 * kDecPerQuarter);   // the decoder warps: selector table in smem
     // Per-unit stage pointers (smem offsets) of unit u; waits for the unit's stage data.
     struct UnitPtr {
       uint32_t p1;     // BlockTile row's plane B1 slice of this unit (B2, B3 at + kUPS*512, 2*kUPS*512)

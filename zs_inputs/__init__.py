@@ -38,6 +38,17 @@ LAYERS = {
     "L70B.O.w8": (8192, 1024),
     "L70B.GateUp.w8": (8192, 7168),
     "L70B.Down.w8": (28672, 1024),
+    # f4: Gemma-3-27B (hidden 5376, intermediate 21504, 32 q / 16 kv heads
+    # of 128), Qwen2.5-7B (hidden 3584, intermediate 18944, 28 q / 4 kv heads of 128);
+    # Mistral-7B-v0.1's linear layers have exactly the LLaMA-3.1-8B shapes above
+    "G3-27B.QKV": (5376, 8192),
+    "G3-27B.O": (4096, 5376),
+    "G3-27B.GateUp": (5376, 43008),
+    "G3-27B.Down": (21504, 5376),
+    "Q2.5-7B.QKV": (3584, 4608),
+    "Q2.5-7B.O": (3584, 3584),
+    "Q2.5-7B.GateUp": (3584, 37888),
+    "Q2.5-7B.Down": (18944, 3584),
     # LM head of LLaMA-3.1-8B (vocabulary 128256, P:493 lists the LM head among the layers)
     "L8B.LMHead": (4096, 128256),
     # fixed-cost probes: one unit (128 x 64) and one 128-row band of K = 4096
