@@ -12,7 +12,8 @@
 //      FragTile row, stored as u16 in a bank-spread table [r8][o].
 //   3. 16 passes of 32 rows: lane -> (row lr = 4 pass + lane/8, FragTile column lane%8),
 //      the branch-free row decoder of zs_device.cuh, and one 16-B store per lane (8 lanes =
-//      one 128-B row segment, fully coalesced).
+//      one 128-B row segment, fully coalesced); passes run in groups of 4 so the rank >= 2
+//      patch is one warp-uniform branch per group.
 #include "zs_device.cuh"
 #include "zs_kernels.h"
 #include "zs_lut.h"
@@ -23,10 +24,6 @@ namespace zs {
 #define ZS_DECOMP_WARPS 16
 #endif
 constexpr int kDecompMaxWarps = ZS_DECOMP_WARPS;   // independent decoder warps per CTA (one CTA per SM)
-#ifndef ZS_DECOMP_UNROLL
-#define ZS_DECOMP_UNROLL 4
-#endif
-constexpr int kDecompUnroll = ZS_DECOMP_UNROLL;   // row passes in flight per warp
 #ifndef ZS_DECOMP_STAGES
 #define ZS_DECOMP_STAGES 2
 #endif
@@ -69,7 +66,9 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
     if (lb) bulk_g2s(st + 1536 + p.hcap, reinterpret_cast<const uint8_t*>(p.l) + a.y, lb, &bars[s], pol);
   };
 
-  int64_t bt = (int64_t)blockIdx.x * nw + warp;
+  // warp-major order: BlockTile g goes to SM g % grid, so the partial last round is spread
+  // over all SMs (at most one extra tile per SM) instead of filling the first SMs' warps
+  int64_t bt = (int64_t)warp * gridDim.x + blockIdx.x;
   if (lane == 0)
     for (int i = 0; i < kDecompStages - 1; ++i)
       if (bt + i * G < nbt) issue(bt + i * G, i);
@@ -129,34 +128,65 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
     }
     __syncwarp();
 
-    // ---- rows
+    // ---- rows: 4 groups of 4 passes; the rank >= 2 patch is a warp-uniform branch per group
     const int64_t br = bt / p.nbc, bc = bt - br * p.nbc;
     const int64_t col = bc * 64 + fc * 8;
-    const bool full_cols = p.vec_ok && (col + 8 <= p.cols);
-#pragma unroll kDecompUnroll
-    for (int pass = 0; pass < 16; ++pass) {
-      const int lr = 4 * pass + (lane >> 3);                 // row inside the BlockTile
-      const int fr = lr >> 3, r8 = lr & 7;
-      const uint32_t o = (uint32_t)((fr >> 1) * 16 + (fr & 1)) + ofc;   // canonical FragTile
-      const uint32_t b1 = st[o * 8 + r8];
-      const uint32_t b2 = st[512 + o * 8 + r8];
-      const uint32_t b3 = st[1024 + o * 8 + r8];
-      const uint32_t m = b1 | b2 | b3;
-      const uint32_t hs = hst[r8 * kHsRow + o];
-      const uint32_t ls = (o * 8 + (uint32_t)r8) * 8u - hs;
-      uint4 v = decode_row_v3(b1, b2, b3, ld_shared_v4(lut_b + 16u * m), Hs + (hs & ~3u), hs * 8u, Ls + 2u * ls, dk);
-      if (lut[m].x & 0x80u)   // >= 3 fallbacks in the row (rank >= 2): rare patch
-        patch_rank2(m, reinterpret_cast<const uint16_t*>(st + 1536 + p.hcap) + ls, v.x, v.y, v.z, v.w);
-      const int64_t row = br * 64 + lr;
-      if (row < p.rows) {
-        uint16_t* dst = p.out + row * p.ld_out + col;
-        if (full_cols) {
-          __stcs(reinterpret_cast<uint4*>(dst), v);   // streaming store: the output is not re-read here
-        } else {
-          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    // interior BlockTile with 16-B aligned rows: no bounds checks, one streaming STG.128 per row
+    const bool interior = p.vec_ok && (bc * 64 + 64 <= p.cols) && (br * 64 + 64 <= p.rows);
+#pragma unroll 1
+    for (int g = 0; g < 4; ++g) {
+      uint4 v[4];
+      uint32_t rare = 0;
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (col + e < p.cols) dst[e] = (uint16_t)(w[e >> 1] >> (16 * (e & 1)));
+      for (int i = 0; i < 4; ++i) {
+        const int lr = 16 * g + 4 * i + (lane >> 3);          // row inside the BlockTile
+        const int fr = lr >> 3, r8 = lr & 7;
+        const uint32_t o = (uint32_t)((fr >> 1) * 16 + (fr & 1)) + ofc;   // canonical FragTile
+        const uint32_t b1 = st[o * 8 + r8];
+        const uint32_t b2 = st[512 + o * 8 + r8];
+        const uint32_t b3 = st[1024 + o * 8 + r8];
+        const uint32_t m = b1 | b2 | b3;
+        const uint32_t hs = hst[r8 * kHsRow + o];
+        const uint32_t ls = (o * 8 + (uint32_t)r8) * 8u - hs;
+        const uint4 ent = ld_shared_v4(lut_b + 16u * m);
+        rare |= ent.x;
+        v[i] = decode_row_v3(b1, b2, b3, ent, Hs + (hs & ~3u), hs * 8u, Ls + 2u * ls, dk);
+      }
+      if (__any_sync(0xFFFFFFFFu, rare & 0x80u)) {
+        // >= 3 fallbacks in some row of the group (rank >= 2): patch those rows
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int lr = 16 * g + 4 * i + (lane >> 3);
+          const int fr = lr >> 3, r8 = lr & 7;
+          const uint32_t o = (uint32_t)((fr >> 1) * 16 + (fr & 1)) + ofc;
+          const uint32_t m = st[o * 8 + r8] | st[512 + o * 8 + r8] | st[1024 + o * 8 + r8];
+          if (lut[m].x & 0x80u) {
+            const uint32_t ls = (o * 8 + (uint32_t)r8) * 8u - hst[r8 * kHsRow + o];
+            patch_rank2(m, reinterpret_cast<const uint16_t*>(st + 1536 + p.hcap) + ls, v[i].x, v[i].y, v[i].z,
+                        v[i].w);
+          }
+        }
+      }
+      const int64_t row0 = br * 64 + 16 * g + (lane >> 3);
+      if (interior) {
+        uint16_t* dst = p.out + row0 * p.ld_out + col;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)   // streaming stores: the output is not re-read here
+          __stcs(reinterpret_cast<uint4*>(dst + (int64_t)(4 * i) * p.ld_out), v[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t row = row0 + 4 * i;
+          if (row >= p.rows) continue;
+          uint16_t* dst = p.out + row * p.ld_out + col;
+          if (p.vec_ok && col + 8 <= p.cols) {
+            __stcs(reinterpret_cast<uint4*>(dst), v[i]);
+          } else {
+            const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (col + e < p.cols) dst[e] = (uint16_t)(w[e >> 1] >> (16 * (e & 1)));
+          }
         }
       }
     }

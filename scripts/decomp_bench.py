@@ -15,12 +15,14 @@ import zs_inputs as G  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--layers", default="L8B.QKV,L8B.O,L8B.GateUp,L8B.Down")
+ap.add_argument("--dist", default="gaussian", choices=["gaussian", "realistic"])
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 l2 = torch.cuda.get_device_properties(dev).L2_cache_size
 for layer in a.layers.split(","):
     K, N = G.LAYERS[layer]
-    w = G.gaussian_bf16(N, K, 0.02, G.seed_of(layer))
+    gen = G.realistic_bf16 if a.dist == "realistic" else G.gaussian_bf16
+    w = gen(N, K, 0.02, seed=G.seed_of(layer))
     zh = Z.encode(w)
     R = max(2, math.ceil(3 * l2 / zh.nbytes()))
     ws = [zh.to(dev) for _ in range(R)]
@@ -37,5 +39,5 @@ for layer in a.layers.split(","):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / a.iters
     byts = zh.nbytes() + 2 * N * K
-    print(json.dumps({"layer": layer, "us": us, "gbs": byts / us / 1e3, "bit_exact": ok,
+    print(json.dumps({"layer": layer, "dist": a.dist, "us": us, "gbs": byts / us / 1e3, "bit_exact": ok,
                       "compressed_mb": zh.nbytes() / 1e6}))
