@@ -28,6 +28,11 @@ def test_sanitizer_clean(tool):
            sys.executable, os.path.join(HERE, "sanitize_target.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
     out = r.stdout + r.stderr
+    if "compute-sanitizer is closed" in out:
+        # the GPU pool disables the tool (runs under it left GPUs needing a reset); the kernels'
+        # own guards (mbarrier watchdogs, host-side shape / capacity checks) and the exact parity
+        # tests are what remain
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert "sanitize target ok" in out, out[-4000:]
     # memcheck / synccheck print "ERROR SUMMARY: 0 errors", racecheck "RACECHECK SUMMARY: 0 hazards
     # displayed (0 errors, 0 warnings)"
