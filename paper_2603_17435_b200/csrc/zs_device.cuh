@@ -83,10 +83,11 @@ __device__ __forceinline__ uint64_t globaltimer_now() {
   return t;
 }
 
-// Wait for the phase with the given parity.  After one probe the waiting warp backs off with
-// nanosleep between probes: a waiting warp shares its SMSP with decoder warps (and the arbiter
-// favours high warp ids, i.e. the control warps), so a tight polling loop would take their
-// issue slots.  The watchdog is time based (checked every 256 probes): > 10 s traps.
+// Wait for the phase with the given parity.  After one probe the waiting warp suspends inside
+// mbarrier.try_wait (suspend-time hint ZS_WAIT_SUSPEND ns; it resumes as soon as the phase
+// completes): a waiting warp shares its SMSP with decoder warps, and a nanosleep polling loop
+// (ZS_WAIT_SUSPEND=0) issued 18% of all the fused kernel's instructions (ncu r02b: 726 K
+// probe iterations per launch).  The watchdog is time based (every 256 probes): > 10 s traps.
 static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity, uint32_t backoff_ns);
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t backoff_ns = 64) {
@@ -105,10 +106,18 @@ __device__ __forceinline__ bool mbar_try_wait_suspend(uint64_t* bar, uint32_t pa
   return ok != 0;
 }
 
+#ifndef ZS_WAIT_SUSPEND
+#define ZS_WAIT_SUSPEND 1000   // > 0: slow waits suspend in mbarrier.try_wait (hint, ns); 0: nanosleep polling
+#endif
 static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity, uint32_t backoff_ns) {
   uint64_t t0 = 0;
+#if ZS_WAIT_SUSPEND
+  (void)backoff_ns;
+  for (uint32_t n = 1; !mbar_try_wait_suspend(bar, parity, ZS_WAIT_SUSPEND); ++n) {
+#else
   for (uint32_t n = 1; !mbar_try_wait(bar, parity); ++n) {
     __nanosleep(backoff_ns);
+#endif
     if ((n & 255u) == 0u) {
       const uint64_t t = globaltimer_now();
       if (t0 == 0) t0 = t;
@@ -233,28 +242,6 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-// thread i of the warp writes 16 consecutive 32-bit columns of TMEM lane (base lane + i)
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, uint4 a, uint4 b, uint4 c, uint4 d) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-          taddr),
-      "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w), "r"(c.x), "r"(c.y), "r"(c.z),
-      "r"(c.w), "r"(d.x), "r"(d.y), "r"(d.z), "r"(d.w)
-      : "memory");
-}
-
-// thread i of the warp writes 32 consecutive 32-bit columns of TMEM lane (base lane + i)
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint4 (&v)[8]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(v[0].x), "r"(v[0].y), "r"(v[0].z), "r"(v[0].w), "r"(v[1].x), "r"(v[1].y), "r"(v[1].z), "r"(v[1].w),
-      "r"(v[2].x), "r"(v[2].y), "r"(v[2].z), "r"(v[2].w), "r"(v[3].x), "r"(v[3].y), "r"(v[3].z), "r"(v[3].w),
-      "r"(v[4].x), "r"(v[4].y), "r"(v[4].z), "r"(v[4].w), "r"(v[5].x), "r"(v[5].y), "r"(v[5].z), "r"(v[5].w),
-      "r"(v[6].x), "r"(v[6].y), "r"(v[6].z), "r"(v[6].w), "r"(v[7].x), "r"(v[7].y), "r"(v[7].z), "r"(v[7].w)
       : "memory");
 }
 
@@ -440,16 +427,6 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
   return v;
 }
 
-// v = [a] if pred (v keeps its value otherwise): a predicated 16-B shared load, so lanes that
-// do not need the entry generate no shared-memory wavefront
-__device__ __forceinline__ void ld_shared_v4_if(uint4& v, uint32_t a, bool pred) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %4, 0;\n\t"
-      "@p ld.shared.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}"
-      : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
-      : "r"((uint32_t)pred), "r"(a));
-}
-
 // Spread of one plane byte b (bit i = element i) into WA / WB positions:
 //   lo = (b & 0xF) * K  and  hi = (b & 0xF0) * K = b * K - lo   (K shifted by the plane's weight)
 // one LOP3 + two full-rate IMADs; no IMAD.HI (a quarter-rate instruction on sm_100a:
@@ -474,63 +451,11 @@ __device__ __forceinline__ void spread_plane_k(uint32_t b, const DecConst& d, ui
 
 // haddr: shared address of the aligned word holding the row's first H byte; hsh8: 8 x that
 // byte's offset (low 5 bits used); laddr: shared address of the row's first fallback value.
-__device__ __forceinline__ uint2 ld_shared_v2(uint32_t a) {
-  uint2 v;
-  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-  return v;
-}
-
 __device__ __forceinline__ uint4 decode_row_v3(uint32_t b1, uint32_t b2, uint32_t b3, uint4 ent, uint32_t haddr,
                                                uint32_t hsh8, uint32_t laddr, const DecConst& d) {
   const uint32_t h0 = ld_shared_u32(haddr), h1 = ld_shared_u32(haddr + 4), h2 = ld_shared_u32(haddr + 8);
   const uint32_t hlo = __funnelshift_r(h0, h1, hsh8);
   const uint32_t hhi = __funnelshift_r(h1, h2, hsh8);
-#if ZS_DEC_BAL
-  const uint32_t lpair = mad_lo(ld_shared_u16(laddr + 2), d.k16, ld_shared_u16(laddr));
-#else
-  const uint32_t lpair = prmt(ld_shared_u16(laddr), ld_shared_u16(laddr + 2), 0x5410u);
-#endif
-  uint32_t l1, u1, l2, u2, l3, u3;
-  spread_plane_k<0>(b1, d, l1, u1);
-  spread_plane_k<1>(b2, d, l2, u2);
-  spread_plane_k<2>(b3, d, l3, u3);
-  // WA = [c0, c2, c1, c3], WB = [c4<<4, c6<<4, c5<<4, c7<<4] bytewise
-  const uint32_t WA = (l1 & 0x01010101u) | (l2 & 0x02020202u) | (l3 & 0x04040404u);
-  const uint32_t WB = (u1 & 0x10101010u) | (u2 & 0x20202020u) | (u3 & 0x40404040u);
-  // (e_base + c) of elements (2j, 2j+1) on bits 7..14 / 23..30 of word j
-#if ZS_DEC_BAL
-  // (IMAD.HI with an addend needs a 64-bit addend register pair: the add goes to IADD3)
-  const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), mul_hi(WA, d.k31) + d.eb7x2, mad_lo(WB, d.k3, d.eb7x2),
-                         mul_hi(WB, d.k27) + d.eb7x2};
-#else
-  const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), (WA >> 1) + d.eb7x2, mad_lo(WB, d.k3, d.eb7x2),
-                         (WB >> 5) + d.eb7x2};
-#endif
-  const uint32_t sel[4] = {ent.x, ent.y, ent.z, ent.w};
-  uint32_t out[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t P = prmt(hlo, hhi, sel[j]);
-    const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);
-#if ZS_DEC_BAL == 1
-    out[j] = prmt(lpair, w, mul_hi(sel[j], d.k16));
-#elif ZS_DEC_BAL == 2
-    out[j] = prmt(lpair, w, j < 2 ? mul_hi(sel[j], d.k16) : (sel[j] >> 16));
-#else
-    out[j] = prmt(lpair, w, sel[j] >> 16);
-#endif
-  }
-  return make_uint4(out[0], out[1], out[2], out[3]);
-}
-
-// H window from two 8-B aligned shared loads (hbyte = shared address of the row's first H byte)
-__device__ __forceinline__ uint4 decode_row_v3h64(uint32_t b1, uint32_t b2, uint32_t b3, uint4 ent, uint32_t hbyte,
-                                                  uint32_t laddr, const DecConst& d) {
-  const uint2 q0 = ld_shared_v2(hbyte & ~7u), q1 = ld_shared_v2((hbyte & ~7u) + 8u);
-  const bool up = (hbyte & 4u) != 0u;
-  const uint32_t w0 = up ? q0.y : q0.x, w1 = up ? q1.x : q0.y, w2 = up ? q1.y : q1.x;
-  const uint32_t hlo = __funnelshift_r(w0, w1, hbyte * 8u);
-  const uint32_t hhi = __funnelshift_r(w1, w2, hbyte * 8u);
 #if ZS_DEC_BAL
   const uint32_t lpair = mad_lo(ld_shared_u16(laddr + 2), d.k16, ld_shared_u16(laddr));
 #else

@@ -50,12 +50,6 @@ namespace zs {
 #ifndef ZS_BACKOFF_DEC
 #define ZS_BACKOFF_DEC 32     // ns between barrier probes of a decoder warp
 #endif
-#ifndef ZS_H64
-#define ZS_H64 0   // 1: the row's H window from two 8-B loads (one wavefront per half-warp) + selects
-#endif
-#ifndef ZS_PRED_SEL
-#define ZS_PRED_SEL 0   // 1: skip the selector-table load for all-in-window rows (predicated LDS)
-#endif
 #ifndef ZS_DEC_PER_Q
 #define ZS_DEC_PER_Q 4   // decoder warps per TMEM lane quarter (static unit assignment, see below)
 #endif
@@ -98,9 +92,6 @@ struct __align__(16) Bars {
   uint32_t last_flag;
 };
 
-#ifndef ZS_REGSPLIT
-#define ZS_REGSPLIT 0   // setmaxnreg 72/40 split: measured 2x slower (spills in the 40-register roles)
-#endif
 #ifndef ZS_TRACE
 #define ZS_TRACE 0   // build with -DZS_TRACE=1 for scripts/trace_gemm.py (costs issue slots)
 #endif
@@ -227,13 +218,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = bars->tmem_base;
   // register budget: 24 decoder warps x 72 + 8 control / epilogue warps x 40 = the 64 K
   // register file (the decoders rematerialise addresses at the 64-register default)
-#if ZS_REGSPLIT
-  if (warp < kWarpEpi0) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 72;");
-  } else {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
-  }
-#endif
   const uint32_t dcols = p.acc_cols;                   // accumulator buffer stride (columns)
   const uint32_t tmem_a = tmem_base + p.n_acc * dcols; // first A slot column
   // accumulator buffer of segment s and the parity of its use (n_acc = 2: double buffered;
@@ -599,18 +583,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint2 s3 = *reinterpret_cast<const uint2*>(P3 + fo * 8);
       const uint32_t mlo = s1.x | s2.x | s3.x, mhi = s1.y | s2.y | s3.y;
       const uint32_t cnt = __popc(mlo) + __popc(mhi);
+      // straight-line (no branch on hh) so that ptxas schedules the scan's loads and popcounts
+      // among the row decode it is placed next to: the first-half total is computed by every
+      // warp and weighted by hh (measured ~1% over the branchy form, r02 A/B)
       uint32_t incl = cnt;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-        if (lane >= d) incl += t;
+        uint32_t t;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "shfl.sync.up.b32 %0|p, %1, %2, 0, -1;\n\t"
+            "@!p mov.b32 %0, 0;\n\t}"
+            : "=r"(t)
+            : "r"(incl), "r"(d));
+        incl += t;
       }
       uint32_t excl = incl - cnt;
-      if (hh) {
+      {
         const uint2 t1 = *reinterpret_cast<const uint2*>(P1 + lane * 8);
         const uint2 t2 = *reinterpret_cast<const uint2*>(P2 + lane * 8);
         const uint2 t3 = *reinterpret_cast<const uint2*>(P3 + lane * 8);
-        excl += __reduce_add_sync(0xFFFFFFFFu, __popc(t1.x | t2.x | t3.x) + __popc(t1.y | t2.y | t3.y));
+        uint32_t first;
+        asm volatile("redux.sync.add.u32 %0, %1, -1;"
+                     : "=r"(first)
+                     : "r"(__popc(t1.x | t2.x | t3.x) + __popc(t1.y | t2.y | t3.y)));
+        excl += first & (0u - (uint32_t)hh);
       }
       const uint32_t bl = bytepop(mlo), bh = bytepop(mhi);
       const uint32_t rp_lo = bl * 0x01010100u;
@@ -620,10 +617,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           make_uint4(prmt(rp_lo, 0u, 0x4140u) + ex2, prmt(rp_lo, 0u, 0x4342u) + ex2, prmt(rp_hi, 0u, 0x4140u) + ex2,
                      prmt(rp_hi, 0u, 0x4342u) + ex2);
     };
-    // Software pipeline: the scan of the warp's NEXT unit runs between the two row passes of
-    // the current one, so its latency chain (loads -> popcounts -> 5 dependent shuffles ->
-    // table) overlaps row-decode work of the same warp instead of idling all four phase-aligned
-    // decoder warps of the SMSP at every stage boundary.
+    // Software pipeline: the scan of the warp's NEXT unit is issued with the second row pass of
+    // the current one (same basic block), so its latency chain (loads -> popcounts -> 5
+    // dependent shuffles -> table) overlaps row-decode work of the same warp instead of idling
+    // all four phase-aligned decoder warps of the SMSP at every stage boundary.
     UnitPtr cur{};
     if (jd < nunits) {
       cur = unit_ptr(jd);
@@ -647,11 +644,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t hb = cur.hb;
 #pragma unroll
       for (int pass = 0; pass < 2; ++pass) {
-        if (pass == 1) {                                          // next unit: wait for its data, scan
-          if (un < nunits) nxt = unit_ptr(un);
-          scan_unit(nxt, rpt + (tb ^ 1u) * kRpBuf);              // (the other table buffer)
+        // next unit: wait for its data here; its scan is issued with this pass's rows (one
+        // basic block).  Past the last unit the current one is re-scanned into the unused buffer.
+        if (pass == 1) nxt = unit_ptr(un < nunits ? un : u);
+        if (p.dbg & 1) {   // timing experiment: no row decode (the scan and the pipeline stay)
+          if (pass == 1) scan_unit(nxt, rpt + (tb ^ 1u) * kRpBuf);
+          continue;
         }
-        if (p.dbg & 1) continue;
         const int lr = 32 * hh + 16 * pass + rl;                    // row inside the BlockTile
         const int fr = lr >> 3, r8 = lr & 7;
         // FragTile of (row, column f): (lr >> 4) * 16 + cf(f) + (fr & 1), cf(f) = (f>>1)*4 + (f&1)*2;
@@ -673,23 +672,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t b2 = pb[cf * 8u + kUPS * 512];
           const uint32_t b3 = pb[cf * 8u + 2 * kUPS * 512];
           const uint32_t m = b1 | b2 | b3;
-#if ZS_PRED_SEL
-          // the all-in-window row (m = 0xFF, ~84% at sigma = 0.02) takes the constant entry
-          uint4 ent = make_uint4(0x76549100u, 0x7654B3A2u, 0x7654D5C4u, 0x7654F7E6u);
-          ld_shared_v4_if(ent, slut_b + m * 16u, m != 0xFFu);
-#else
           const uint4 ent = ld_shared_v4(slut_b + m * 16u);
-#endif
           rare |= ent.x;
-#if ZS_H64
-          v[qq] = decode_row_v3h64(b1, b2, b3, ent, sbase + hs_abs, sbase + la0 + 128u * cf - 2u * hs_abs, dk);
-#else
           v[qq] = decode_row_v3(b1, b2, b3, ent, sbase + (hs_abs & ~3u), hs_abs * 8u,
                                 sbase + la0 + 128u * cf - 2u * hs_abs, dk);
-#endif
+        }
+        if (pass == 1) scan_unit(nxt, rpt + (tb ^ 1u) * kRpBuf);   // (the other table buffer)
+        if (p.dbg & 2) {
+          uint32_t x = 0;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) x ^= v[qq].x ^ v[qq].y ^ v[qq].z ^ v[qq].w;
+          if (x == 0x9E3779B9u) p.counters[0] = x;   // keeps the decode live
+        } else {
+          // TMEM lanes 32q + 16 pass + (0..15); half-warp kh writes columns 16 kh .. 16 kh + 15
+          tmem_st16x2(taddr0 + ((uint32_t)(16 * pass) << 16), v[0], v[1], v[2], v[3]);
         }
         if (__any_sync(0xFFFFFFFFu, rare & 0x80u)) {
-          // rare: a row of this pass has >= 3 fallbacks (rank >= 2); warp-uniform branch
+          // rare: a row of this pass has >= 3 fallbacks (rank >= 2); warp-uniform branch.  The
+          // fast-path rows are already in TMEM (storing them before this check lets ptxas
+          // decode straight into the store's registers); the patched rows are stored again
+          // once the first stores have completed.
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq) {
             const uint32_t cf = (uint32_t)((qq >> 1) * 4 + (qq & 1) * 2);
@@ -699,14 +701,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               patch_rank2(m, reinterpret_cast<const uint16_t*>(smem + la0 + 128u * cf - 2u * hs_abs), v[qq].x,
                           v[qq].y, v[qq].z, v[qq].w);
           }
-        }
-        if (p.dbg & 2) {
-          uint32_t x = 0;
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) x ^= v[qq].x ^ v[qq].y ^ v[qq].z ^ v[qq].w;
-          if (x == 0x9E3779B9u) p.counters[0] = x;   // keeps the decode live
-        } else {
-          // TMEM lanes 32q + 16 pass + (0..15); half-warp kh writes columns 16 kh .. 16 kh + 15
+          tmem_wait_st();
           tmem_st16x2(taddr0 + ((uint32_t)(16 * pass) << 16), v[0], v[1], v[2], v[3]);
         }
       }
