@@ -133,21 +133,6 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
     const int64_t col = bc * 64 + fc * 8;
     // interior BlockTile with 16-B aligned rows: no bounds checks, one streaming STG.128 per row
     const bool interior = p.vec_ok && (bc * 64 + 64 <= p.cols) && (br * 64 + 64 <= p.rows);
-    // >= 3 fallbacks in some row of the group (rank >= 2): patch those rows (warp-uniform call)
-    auto patch_group = [&](int g, uint4 (&v)[4]) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int lr = 16 * g + 4 * i + (lane >> 3);
-        const int fr = lr >> 3, r8 = lr & 7;
-        const uint32_t o = (uint32_t)((fr >> 1) * 16 + (fr & 1)) + ofc;
-        const uint32_t m = st[o * 8 + r8] | st[512 + o * 8 + r8] | st[1024 + o * 8 + r8];
-        if (lut[m].x & 0x80u) {
-          const uint32_t ls = (o * 8 + (uint32_t)r8) * 8u - hst[r8 * kHsRow + o];
-          patch_rank2(m, reinterpret_cast<const uint16_t*>(st + 1536 + p.hcap) + ls, v[i].x, v[i].y, v[i].z,
-                      v[i].w);
-        }
-      }
-    };
 #pragma unroll 1
     for (int g = 0; g < 4; ++g) {
       uint4 v[4];
@@ -167,24 +152,28 @@ __global__ void __launch_bounds__(32 * kDecompMaxWarps, 1) decompress_kernel(Dec
         rare |= ent.x;
         v[i] = decode_row_v3(b1, b2, b3, ent, Hs + (hs & ~3u), hs * 8u, Ls + 2u * ls, dk);
       }
+      if (__any_sync(0xFFFFFFFFu, rare & 0x80u)) {
+        // >= 3 fallbacks in some row of the group (rank >= 2): patch those rows
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int lr = 16 * g + 4 * i + (lane >> 3);
+          const int fr = lr >> 3, r8 = lr & 7;
+          const uint32_t o = (uint32_t)((fr >> 1) * 16 + (fr & 1)) + ofc;
+          const uint32_t m = st[o * 8 + r8] | st[512 + o * 8 + r8] | st[1024 + o * 8 + r8];
+          if (lut[m].x & 0x80u) {
+            const uint32_t ls = (o * 8 + (uint32_t)r8) * 8u - hst[r8 * kHsRow + o];
+            patch_rank2(m, reinterpret_cast<const uint16_t*>(st + 1536 + p.hcap) + ls, v[i].x, v[i].y, v[i].z,
+                        v[i].w);
+          }
+        }
+      }
       const int64_t row0 = br * 64 + 16 * g + (lane >> 3);
-      const bool any_rare = __any_sync(0xFFFFFFFFu, rare & 0x80u);
       if (interior) {
-        // the fast-path rows are stored first (ptxas then decodes straight into the store
-        // registers); rows with >= 3 fallbacks are patched and stored again (same thread, same
-        // address: the second store wins)
         uint16_t* dst = p.out + row0 * p.ld_out + col;
 #pragma unroll
         for (int i = 0; i < 4; ++i)   // streaming stores: the output is not re-read here
           __stcs(reinterpret_cast<uint4*>(dst + (int64_t)(4 * i) * p.ld_out), v[i]);
-        if (any_rare) {
-          patch_group(g, v);
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            __stcs(reinterpret_cast<uint4*>(dst + (int64_t)(4 * i) * p.ld_out), v[i]);
-        }
       } else {
-        if (any_rare) patch_group(g, v);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int64_t row = row0 + 4 * i;

@@ -111,7 +111,13 @@ __device__ __forceinline__ bool mbar_try_wait_suspend(uint64_t* bar, uint32_t pa
 #endif
 static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity, uint32_t backoff_ns) {
   uint64_t t0 = 0;
-#if ZS_WAIT_SUSPEND
+#if ZS_WAIT_SUSPEND == 2
+  // hybrid: long back-offs (the control warps, which mostly wait for the decoders) sleep between
+  // probes; short ones (decoders) suspend in try_wait
+  for (uint32_t n = 1; !(backoff_ns >= 128u ? mbar_try_wait(bar, parity) : mbar_try_wait_suspend(bar, parity, 1000u));
+       ++n) {
+    if (backoff_ns >= 128u) __nanosleep(backoff_ns);
+#elif ZS_WAIT_SUSPEND
   (void)backoff_ns;
   for (uint32_t n = 1; !mbar_try_wait_suspend(bar, parity, ZS_WAIT_SUSPEND); ++n) {
 #else
@@ -435,12 +441,13 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
 // Pipe balance of the row decoder (sm_100a: LOP3 / PRMT / SHF and IMAD issue at 0.5 warp-instr
 // per cycle per SMSP, IMAD.HI at 0.24; scripts/pipe_probe.cu).  2: shifts split between the
 // FMA pipe (IMAD.HI) and the ALU pipe (SHF) so both pipes carry about the same cycles per row;
-// 1: all shifts on the FMA pipe; 0: all shifts on the ALU pipe.
+// 1: all shifts on the FMA pipe; 0: all shifts on the ALU pipe; 3: as 2 but the odd exponent
+// words by LEA.HI (ALU) instead of IMAD.HI; 4: as 3 and the plane spread masks with LOP3.
 #define ZS_DEC_BAL 2
 #endif
 template <int kShift>
 __device__ __forceinline__ void spread_plane_k(uint32_t b, const DecConst& d, uint32_t& lo, uint32_t& hi) {
-#if ZS_DEC_BAL
+#if ZS_DEC_BAL && ZS_DEC_BAL != 4
   hi = mul_hi(b, d.k28) * (ZS_KSPREAD << (4 + kShift));   // (b >> 4) on the FMA pipe
   lo = b * (ZS_KSPREAD << kShift) - hi;
 #else
@@ -469,7 +476,11 @@ __device__ __forceinline__ uint4 decode_row_v3(uint32_t b1, uint32_t b2, uint32_
   const uint32_t WA = (l1 & 0x01010101u) | (l2 & 0x02020202u) | (l3 & 0x04040404u);
   const uint32_t WB = (u1 & 0x10101010u) | (u2 & 0x20202020u) | (u3 & 0x40404040u);
   // (e_base + c) of elements (2j, 2j+1) on bits 7..14 / 23..30 of word j
-#if ZS_DEC_BAL
+#if ZS_DEC_BAL >= 3
+  // odd words as (W >> s) + EB: one LEA.HI each on the ALU pipe (no quarter-rate IMAD.HI)
+  const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), (WA >> 1) + d.eb7x2, mad_lo(WB, d.k3, d.eb7x2),
+                         (WB >> 5) + d.eb7x2};
+#elif ZS_DEC_BAL
   // (IMAD.HI with an addend needs a 64-bit addend register pair: the add goes to IADD3)
   const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), mul_hi(WA, d.k31) + d.eb7x2, mad_lo(WB, d.k3, d.eb7x2),
                          mul_hi(WB, d.k27) + d.eb7x2};
@@ -485,7 +496,7 @@ __device__ __forceinline__ uint4 decode_row_v3(uint32_t b1, uint32_t b2, uint32_
     const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);
 #if ZS_DEC_BAL == 1
     out[j] = prmt(lpair, w, mul_hi(sel[j], d.k16));
-#elif ZS_DEC_BAL == 2
+#elif ZS_DEC_BAL >= 2
     out[j] = prmt(lpair, w, j < 2 ? mul_hi(sel[j], d.k16) : (sel[j] >> 16));
 #else
     out[j] = prmt(lpair, w, sel[j] >> 16);
