@@ -441,13 +441,14 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
 // Pipe balance of the row decoder (sm_100a: LOP3 / PRMT / SHF and IMAD issue at 0.5 warp-instr
 // per cycle per SMSP, IMAD.HI at 0.24; scripts/pipe_probe.cu).  2: shifts split between the
 // FMA pipe (IMAD.HI) and the ALU pipe (SHF) so both pipes carry about the same cycles per row;
-// 1: all shifts on the FMA pipe; 0: all shifts on the ALU pipe; 3: as 2 but the odd exponent
-// words by LEA.HI (ALU) instead of IMAD.HI; 4: as 3 and the plane spread masks with LOP3.
-#define ZS_DEC_BAL 2
+// 1: all shifts on the FMA pipe; 0: all shifts on the ALU pipe; 3 (default): as 2 but the odd
+// exponent words by LEA.HI (ALU) instead of IMAD.HI (8B GateUp M = 32: 69.2 -> 67.5 us, r02 it4);
+// 4: as 3 and the plane spread masks with LOP3; 5: as 4 and every selector shift on SHF.
+#define ZS_DEC_BAL 3
 #endif
 template <int kShift>
 __device__ __forceinline__ void spread_plane_k(uint32_t b, const DecConst& d, uint32_t& lo, uint32_t& hi) {
-#if ZS_DEC_BAL && ZS_DEC_BAL != 4
+#if ZS_DEC_BAL && ZS_DEC_BAL != 4 && ZS_DEC_BAL != 5
   hi = mul_hi(b, d.k28) * (ZS_KSPREAD << (4 + kShift));   // (b >> 4) on the FMA pipe
   lo = b * (ZS_KSPREAD << kShift) - hi;
 #else
@@ -496,6 +497,8 @@ __device__ __forceinline__ uint4 decode_row_v3(uint32_t b1, uint32_t b2, uint32_
     const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);
 #if ZS_DEC_BAL == 1
     out[j] = prmt(lpair, w, mul_hi(sel[j], d.k16));
+#elif ZS_DEC_BAL >= 5
+    out[j] = prmt(lpair, w, sel[j] >> 16);
 #elif ZS_DEC_BAL >= 2
     out[j] = prmt(lpair, w, j < 2 ? mul_hi(sel[j], d.k16) : (sel[j] >> 16));
 #else
