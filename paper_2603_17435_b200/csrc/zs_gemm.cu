@@ -54,6 +54,10 @@ namespace zs {
 #define ZS_DEC_PER_Q 4   // decoder warps per TMEM lane quarter (static unit assignment, see below)
 #endif
 constexpr int kDecPerQuarter = ZS_DEC_PER_Q;
+// one decoder warp per unit of a stage: with more warps than units per stage a warp's next unit
+// can sit two stages ahead of its current one (measured: D = 5 deadlocks on the 3-slot
+// compressed ring at M = 200 and is 25% slower where it completes, r02 it6)
+static_assert(kDecPerQuarter == 4, "the static unit assignment assumes one decoder warp per unit of a stage");
 constexpr int kWarpDec0 = 0;                       // warps 0..4D-1: decoders (lane quarter = warp % 4)
 constexpr int kWarpEpi0 = 4 * kDecPerQuarter;      // 4 epilogue warps (TMEM lane quarters)
 constexpr int kWarpAlloc = kWarpEpi0 + 4;
