@@ -12,7 +12,7 @@ import zs_inputs as G  # noqa: E402
 dev = torch.device("cuda:0")
 ok = True
 for (N, K, M) in [(1024, 4096, 32), (640, 1000, 17), (28672, 4096, 32), (4096, 14336, 1), (28672, 4096, 200),
-                  (14336, 4096, 256), (6144, 4096, 8)]:
+                  (14336, 4096, 256), (6144, 4096, 8), (28672, 4096, 128), (14336, 4096, 96)]:
     w = G.integer_weights(N, K, seed=G.seed_of(f"qc.W{N}.{K}"))
     x = G.integer_activations(M, K, seed=G.seed_of(f"qc.X{M}.{K}"))
     wf = G.bf16_bits_to_fp32(w).astype(np.int64)
