@@ -188,9 +188,6 @@ extern "C" zs_status zs_decompress(const zs_tensor* w, uint16_t* out, int64_t ld
   return ZS_OK;
 }
 
-#ifndef ZS_SPLIT3
-#define ZS_SPLIT3 0   // > 0: prefer 3 compressed stages with that many X tiles over 2 stages with 4
-#endif
 #ifndef ZS_XTILES_MAX
 #define ZS_XTILES_MAX 12   // X tiles in the ring at most (L2-sourced; 3 stages of 4 units)
 #endif
@@ -320,11 +317,7 @@ static zs_status gemm_core(const uint16_t* x, int64_t ldx, const zs_tensor* w, u
     const uint32_t cmax = std::min<uint32_t>((uint32_t)zs::gemm_max_cslots(), g_max_cslots);
     // preference: 3 compressed stages with >= 4 X tiles (measured best at small M; a 4th
     // stage measured no change), then 2 stages with >= 4 tiles, then 2 with >= 2 tiles
-#if ZS_SPLIT3
-    static const uint32_t pref[][2] = {{3, 4}, {3, ZS_SPLIT3}, {2, 4}, {2, 2}, {1, 2}};
-#else
     static const uint32_t pref[][2] = {{3, 4}, {2, 4}, {2, 2}, {1, 2}};
-#endif
     for (const auto& pr : pref) {
       const uint32_t c = std::min(pr[0], cmax);
       if (base + c * cs + pr[1] * xs > budget) continue;

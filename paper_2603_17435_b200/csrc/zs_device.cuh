@@ -508,46 +508,5 @@ __device__ __forceinline__ uint4 decode_row_v3(uint32_t b1, uint32_t b2, uint32_
   return make_uint4(out[0], out[1], out[2], out[3]);
 }
 
-// decode_row_v3 with the fallback-merge selectors from a second table (lent.j = ent.j >> 16)
-__device__ __forceinline__ uint4 decode_row_v3l(uint32_t b1, uint32_t b2, uint32_t b3, uint4 ent, uint4 lent, uint32_t haddr,
-                                               uint32_t hsh8, uint32_t laddr, const DecConst& d) {
-  const uint32_t h0 = ld_shared_u32(haddr), h1 = ld_shared_u32(haddr + 4), h2 = ld_shared_u32(haddr + 8);
-  const uint32_t hlo = __funnelshift_r(h0, h1, hsh8);
-  const uint32_t hhi = __funnelshift_r(h1, h2, hsh8);
-#if ZS_DEC_BAL
-  const uint32_t lpair = mad_lo(ld_shared_u16(laddr + 2), d.k16, ld_shared_u16(laddr));
-#else
-  const uint32_t lpair = prmt(ld_shared_u16(laddr), ld_shared_u16(laddr + 2), 0x5410u);
-#endif
-  uint32_t l1, u1, l2, u2, l3, u3;
-  spread_plane_k<0>(b1, d, l1, u1);
-  spread_plane_k<1>(b2, d, l2, u2);
-  spread_plane_k<2>(b3, d, l3, u3);
-  // WA = [c0, c2, c1, c3], WB = [c4<<4, c6<<4, c5<<4, c7<<4] bytewise
-  const uint32_t WA = (l1 & 0x01010101u) | (l2 & 0x02020202u) | (l3 & 0x04040404u);
-  const uint32_t WB = (u1 & 0x10101010u) | (u2 & 0x20202020u) | (u3 & 0x40404040u);
-  // (e_base + c) of elements (2j, 2j+1) on bits 7..14 / 23..30 of word j
-#if ZS_DEC_BAL >= 3
-  // odd words as (W >> s) + EB: one LEA.HI each on the ALU pipe (no quarter-rate IMAD.HI)
-  const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), (WA >> 1) + d.eb7x2, mad_lo(WB, d.k3, d.eb7x2),
-                         (WB >> 5) + d.eb7x2};
-#elif ZS_DEC_BAL
-  // (IMAD.HI with an addend needs a 64-bit addend register pair: the add goes to IADD3)
-  const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), mul_hi(WA, d.k31) + d.eb7x2, mad_lo(WB, d.k3, d.eb7x2),
-                         mul_hi(WB, d.k27) + d.eb7x2};
-#else
-  const uint32_t E[4] = {mad_lo(WA, d.k7, d.eb7x2), (WA >> 1) + d.eb7x2, mad_lo(WB, d.k3, d.eb7x2),
-                         (WB >> 5) + d.eb7x2};
-#endif
-  const uint32_t sel[4] = {ent.x, ent.y, ent.z, ent.w};
-  uint32_t out[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t P = prmt(hlo, hhi, sel[j]);
-    const uint32_t w = bitsel<0x807F807Fu>(P, E[j]);
-    out[j] = prmt(lpair, w, (&lent.x)[j]);
-  }
-  return make_uint4(out[0], out[1], out[2], out[3]);
-}
 
 }  // namespace zs

@@ -50,13 +50,7 @@ namespace zs {
 #ifndef ZS_BACKOFF_DEC
 #define ZS_BACKOFF_DEC 32     // ns between barrier probes of a decoder warp
 #endif
-#ifndef ZS_INCR
-#define ZS_INCR 0   // 1: ring slots / parities of the decoder loop tracked incrementally (no divisions)
-#endif
-#ifndef ZS_LSEL
-#define ZS_LSEL 0   // 1: fallback-merge selectors in a second smem table (no per-row selector shifts)
-#endif
-constexpr uint32_t kLutBytes = ZS_LSEL ? 8192u : 4096u;
+constexpr uint32_t kLutBytes = 4096u;   // selector table (a second table of fallback selectors measured 4% slower)
 #ifndef ZS_DEC_PER_Q
 #define ZS_DEC_PER_Q 4   // decoder warps per TMEM lane quarter (static unit assignment, see below)
 #endif
@@ -83,11 +77,8 @@ constexpr uint32_t kStageMeta = 128;               // see the stage header layou
 constexpr uint32_t kBtPlaneStride = 3 * kUPS * 512 + 32;
 constexpr uint32_t kStagePlanes = 2 * kBtPlaneStride;
 constexpr uint32_t kTmemCols = 512;
-#ifndef ZS_RT32
-#define ZS_RT32 0   // 1: the row table holds absolute u32 smem addresses of the rows' first H byte
-#endif
-// row table: 32 FragTiles x 8 rows x u16 (+ pad), or x u32 with 64 B of pad per 8 FragTiles
-constexpr uint32_t kRpBuf = ZS_RT32 ? 1280u : 32 * 16 + 64;
+// row table: 32 FragTiles x 8 rows x u16 (+ pad)
+constexpr uint32_t kRpBuf = 32 * 16 + 64;
 constexpr uint32_t kRpWarp = 2 * kRpBuf;             // per decoder warp: double-buffered (software pipeline)
 constexpr uint32_t kRpTabBytes = 4 * kDecPerQuarter * kRpWarp;
 
@@ -561,9 +552,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (tid < 256) {
       const uint4 e = __ldg(&c_lut[tid]);
       slut[tid] = e;
-#if ZS_LSEL
-      slut[256 + tid] = make_uint4(e.x >> 16, e.y >> 16, e.z >> 16, e.w >> 16);
-#endif
     }
     named_bar_sync(4, 32 * 4 * kDecPerQuarter);   // the decoder warps: selector table in smem
     // Per-unit stage pointers (smem offsets) of unit u; waits for the unit's stage data.
@@ -573,14 +561,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t lb;     // L segment base
       uint32_t slot;   // compressed ring slot
     };
-#if ZS_INCR
-    // (slot, parity) of the compressed-ring stage holding unit u, tracked incrementally by the caller
-    auto unit_ptr = [&](int u, uint32_t slot, uint32_t par) {
-      const uint32_t j = (uint32_t)u % kUPS;
-      const uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
-      const uint32_t* meta = reinterpret_cast<const uint32_t*>(cs);
-      mbar_wait(&bars->full_c[slot], par, ZS_BACKOFF_DEC);
-#else
     auto unit_ptr = [&](int u) {
       const uint32_t st = (uint32_t)u / kUPS, j = (uint32_t)u % kUPS;
       const uint32_t stc = fastdiv(st, S_c, p.cdiv_magic);
@@ -588,7 +568,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
       const uint32_t* meta = reinterpret_cast<const uint32_t*>(cs);
       mbar_wait(&bars->full_c[slot], stc & 1u, ZS_BACKOFF_DEC);
-#endif
       if (lane == 0) trace_ev(p.trace, u, 7 + q);
       // an absent BlockTile row b (odd row count) is aliased to row a: its rows decode valid
       // bytes into TMEM lanes whose outputs (rows >= N) the epilogue never stores
@@ -642,49 +621,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t bl = bytepop(mlo), bh = bytepop(mhi);
       const uint32_t rp_lo = bl * 0x01010100u;
       const uint32_t rp_hi = bh * 0x01010100u + ((bl * 0x01010101u) >> 24) * 0x01010101u;
-#if ZS_RT32
-      // absolute shared address of each of the FragTile's 8 rows' first H byte
-      const uint32_t hb0 = sbase + up.hb + excl;
-      uint4* w32 = reinterpret_cast<uint4*>(tab + (uint32_t)lane * 32u + ((uint32_t)lane >> 3) * 64u);
-      w32[0] = make_uint4(hb0 + prmt(rp_lo, 0u, 0x4440u), hb0 + prmt(rp_lo, 0u, 0x4441u), hb0 + prmt(rp_lo, 0u, 0x4442u),
-                          hb0 + prmt(rp_lo, 0u, 0x4443u));
-      w32[1] = make_uint4(hb0 + prmt(rp_hi, 0u, 0x4440u), hb0 + prmt(rp_hi, 0u, 0x4441u), hb0 + prmt(rp_hi, 0u, 0x4442u),
-                          hb0 + prmt(rp_hi, 0u, 0x4443u));
-#else
       const uint32_t ex2 = excl * 0x10001u;
       *reinterpret_cast<uint4*>(tab + rp_wr) =
           make_uint4(prmt(rp_lo, 0u, 0x4140u) + ex2, prmt(rp_lo, 0u, 0x4342u) + ex2, prmt(rp_hi, 0u, 0x4140u) + ex2,
                      prmt(rp_hi, 0u, 0x4342u) + ex2);
-#endif
     };
     // Software pipeline: the scan of the warp's NEXT unit is issued with the second row pass of
     // the current one (same basic block), so its latency chain (loads -> popcounts -> 5
     // dependent shuffles -> table) overlaps row-decode work of the same warp instead of idling
     // all four phase-aligned decoder warps of the SMSP at every stage boundary.
     UnitPtr cur{};
-#if ZS_INCR
-    uint32_t c_slot = 0, c_par = 0;   // ring position of the current unit's stage (stage 0 first)
-    uint32_t astg = 0, ag = 0;        // TMEM A stage of the current unit and its use count
-    if (jd < nunits) {
-      cur = unit_ptr(jd, 0u, 0u);
-#else
     if (jd < nunits) {
       cur = unit_ptr(jd);
-#endif
       scan_unit(cur, rpt);
     }
     uint32_t tb = 0;                              // row table buffer of the current unit
     for (int u = jd; u < nunits; u += kDecPerQuarter, tb ^= 1u) {
       const int un = u + kDecPerQuarter;
-#if ZS_INCR
-      const uint32_t j = (uint32_t)jd;                     // u % kUPS (one decoder warp per unit of a stage)
-      uint32_t n_slot = c_slot + 1u, n_par = c_par;        // ring position of the next stage
-      if (n_slot == S_c) { n_slot = 0u; n_par ^= 1u; }
-#else
       const uint32_t st = (uint32_t)u / kUPS, j = (uint32_t)u % kUPS;
       const uint32_t ag = fastdiv(st, SAS, p.adiv_magic);  // use count of the A stage
       const uint32_t astg = st - ag * SAS;                 // TMEM A stage of this unit
-#endif
       const uint32_t a = astg * kUPS + j;                  // TMEM A slot of this unit
       const uint8_t* tab = rpt + tb * kRpBuf;
       __syncwarp();                                        // this unit's row table is written
@@ -699,14 +655,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int pass = 0; pass < 2; ++pass) {
         // next unit: wait for its data here; its scan is issued with this pass's rows (one
         // basic block).  Past the last unit the current one is re-scanned into the unused buffer.
-#if ZS_INCR
-        if (pass == 1) {
-          const bool hn = un < nunits;
-          nxt = unit_ptr(hn ? un : u, hn ? n_slot : c_slot, hn ? n_par : c_par);
-        }
-#else
         if (pass == 1) nxt = unit_ptr(un < nunits ? un : u);
-#endif
         if (p.dbg & 1) {   // timing experiment: no row decode (the scan and the pipeline stay)
           if (pass == 1) scan_unit(nxt, rpt + (tb ^ 1u) * kRpBuf);
           continue;
@@ -718,45 +667,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t ob = (uint32_t)((lr >> 4) * 16 + (fr & 1) + 8 * kh);   // FragTile for qq = 0
         const uint32_t ol = ob - 32u * hh;                                    // local FragTile
         const uint8_t* pb = smem + cur.p1 + ob * 8u + (uint32_t)r8;           // plane byte, qq = 0
-#if ZS_RT32
-        const uint8_t* rb = tab + ol * 32u + (ol >> 3) * 64u + 4u * (uint32_t)r8;
-#else
         const uint8_t* rb = tab + ol * 16u + (ol >> 3) * 16u + 2u * (uint32_t)r8;
-#endif
         // fallback values of the row start at element 8*(o*8 + r8) - (its H offset) of the L segment
         const uint32_t la0 = cur.lb + 2u * hb + 16u * (ob * 8u + (uint32_t)r8);
-#if ZS_RT32
-        const uint32_t lk = 3u * sbase + la0;   // laddr = lk + 128 cf - 2 (sbase + hs_abs)
-#endif
         uint4 v[4];
         uint32_t rare = 0;
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
           const uint32_t cf = (uint32_t)((qq >> 1) * 4 + (qq & 1) * 2);
           // table offset of FragTile ol + cf: cf in {0,2,4,6} never crosses an 8-FragTile pad
-#if ZS_RT32
-          const uint32_t habs = *reinterpret_cast<const uint32_t*>(rb + cf * 32u);   // sbase + hs_abs
-          const uint32_t hs_abs = habs - sbase;
-#else
           const uint32_t hs_abs = hb + *reinterpret_cast<const uint16_t*>(rb + cf * 16u);
-#endif
           const uint32_t b1 = pb[cf * 8u];
           const uint32_t b2 = pb[cf * 8u + kUPS * 512];
           const uint32_t b3 = pb[cf * 8u + 2 * kUPS * 512];
           const uint32_t m = b1 | b2 | b3;
           const uint4 ent = ld_shared_v4(slut_b + m * 16u);
           rare |= ent.x;
-#if ZS_RT32
-          const uint32_t haddr = habs & ~3u, hsh8 = habs * 8u, laddr = lk + 128u * cf - 2u * habs;
-#else
           const uint32_t haddr = sbase + (hs_abs & ~3u), hsh8 = hs_abs * 8u, laddr = sbase + la0 + 128u * cf - 2u * hs_abs;
-#endif
-#if ZS_LSEL
-          const uint4 lent = ld_shared_v4(slut_b + 4096u + m * 16u);
-          v[qq] = decode_row_v3l(b1, b2, b3, ent, lent, haddr, hsh8, laddr, dk);
-#else
           v[qq] = decode_row_v3(b1, b2, b3, ent, haddr, hsh8, laddr, dk);
-#endif
         }
         if (pass == 1) scan_unit(nxt, rpt + (tb ^ 1u) * kRpBuf);   // (the other table buffer)
         if (p.dbg & 2) {
@@ -776,11 +704,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq) {
             const uint32_t cf = (uint32_t)((qq >> 1) * 4 + (qq & 1) * 2);
-#if ZS_RT32
-            const uint32_t hs_abs = *reinterpret_cast<const uint32_t*>(rb + cf * 32u) - sbase;
-#else
             const uint32_t hs_abs = hb + *reinterpret_cast<const uint16_t*>(rb + cf * 16u);
-#endif
             const uint32_t m = pb[cf * 8u] | pb[cf * 8u + kUPS * 512] | pb[cf * 8u + 2 * kUPS * 512];
             if (slut[m].x & 0x80u)
               patch_rank2(m, reinterpret_cast<const uint16_t*>(smem + la0 + 128u * cf - 2u * hs_abs), v[qq].x,
@@ -799,11 +723,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (lane == 0) trace_ev(p.trace, u, 2 + q);
       if (lane == 0) mbar_arrive(&bars->empty_c[cur.slot]);   // all lanes are done with the stage
       cur = nxt;
-#if ZS_INCR
-      c_slot = n_slot;
-      c_par = n_par;
-      if (++astg == SAS) { astg = 0u; ++ag; }
-#endif
     }
     // A partial last stage still needs its 16 afull arrivals: this warp's units past the end
     // that fall in that stage arrive without decoding (after the slot's previous use is
