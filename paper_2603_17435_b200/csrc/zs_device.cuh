@@ -42,11 +42,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
-// raise the expected transaction count of the current phase without arriving
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
 // try_wait without a suspend hint: the hardware blocks for a short, system-defined time
 // and returns as soon as the phase completes -- used on the critical path.
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {

@@ -51,9 +51,6 @@ namespace zs {
 #define ZS_BACKOFF_DEC 32     // ns between barrier probes of a decoder warp
 #endif
 constexpr uint32_t kLutBytes = 4096u;   // selector table (a second table of fallback selectors measured 4% slower)
-#ifndef ZS_EARLY
-#define ZS_EARLY 0   // 1: the first ring stages' plane slices are requested before the offsets load
-#endif
 #ifndef ZS_DEC_PER_Q
 #define ZS_DEC_PER_Q 4   // decoder warps per TMEM lane quarter (static unit assignment, see below)
 #endif
@@ -246,53 +243,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const ulonglong2* off2 = reinterpret_cast<const ulonglong2*>(p.offsets);
     const int quad = lane / kUPS, qi = lane % kUPS;   // lane group of a stage / unit in it
     uint32_t slot = 0, eph = 1;   // ring slot / empty-barrier parity of the next stage
-#if ZS_EARLY
-    // The ring starts empty: the plane slices of the first S_c stages (their addresses need no
-    // offsets) are requested before the offsets load, under a bare expect_tx; the H / L copies
-    // and the stage's single arrival follow once the offsets are known (the phase cannot
-    // complete before that arrival).
-    const int nearly = min(nstages, (int)S_c);
-    if (!(p.dbg & 8)) {
-      const int it = lane;
-      const bool valid = it < nunits && it < nearly * kUPS;
-      const uint32_t kk = kc0 + (uint32_t)it;
-      const uint32_t band = band0 + kk / nbc, kc = kk % nbc;
-      const uint32_t bta = 2u * band * nbc + kc;
-      const bool has_b = valid && (2u * band + 1u < nbr);
-      uint32_t pbytes = valid ? (has_b ? 3072u : 1536u) : 0u;
-#pragma unroll
-      for (int d = 1; d < kUPS; d <<= 1) pbytes += __shfl_xor_sync(0xFFFFFFFFu, pbytes, d);
-      const uint32_t band_prev = __shfl_up_sync(0xFFFFFFFFu, band, 1);
-      const bool run_start = valid && (qi == 0 || band_prev != band);
-      const uint32_t starts = __ballot_sync(0xFFFFFFFFu, run_start);
-      const uint32_t validm = __ballot_sync(0xFFFFFFFFu, valid);
-      const uint32_t quad_mask = ((1u << kUPS) - 1u) << (kUPS * quad);
-      const uint32_t later = starts & quad_mask & ~((2u << lane) - 1u);
-      const uint32_t qvalid = validm & quad_mask;
-      const int qlast = qvalid ? 31 - __clz(qvalid) : lane;
-      const int rend = later ? (__ffs(later) - 2) : qlast;
-      const uint32_t nrun = (uint32_t)(rend - lane + 1);
-      if (quad < nearly) {
-        uint64_t* fb = &bars->full_c[quad];
-        if (qi == 0) mbar_expect_tx(fb, pbytes);
-        __syncwarp(0xFFFFFFFFu >> (32 - kUPS * nearly));
-        if (run_start) {
-          uint8_t* planes = cslots + (size_t)quad * p.cslot_bytes + kStageMeta;
-          const uint32_t pb = nrun * 512u, po = (uint32_t)qi * 512u;
-          bulk_g2s(planes + 0 * (kUPS * 512) + po, p.b1 + (size_t)bta * 64, pb, fb, pol);
-          bulk_g2s(planes + 1 * (kUPS * 512) + po, p.b2 + (size_t)bta * 64, pb, fb, pol);
-          bulk_g2s(planes + 2 * (kUPS * 512) + po, p.b3 + (size_t)bta * 64, pb, fb, pol);
-          if (has_b) {
-            const size_t btb = (size_t)bta + nbc;
-            bulk_g2s(planes + kBtPlaneStride + 0 * (kUPS * 512) + po, p.b1 + btb * 64, pb, fb, pol);
-            bulk_g2s(planes + kBtPlaneStride + 1 * (kUPS * 512) + po, p.b2 + btb * 64, pb, fb, pol);
-            bulk_g2s(planes + kBtPlaneStride + 2 * (kUPS * 512) + po, p.b3 + btb * 64, pb, fb, pol);
-          }
-        }
-      }
-      __syncwarp();
-    }
-#endif
     for (int b0 = 0; b0 < nunits; b0 += 32) {
       const int it = b0 + lane;
       const bool valid = it < nunits;
@@ -323,13 +273,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t stage_bytes = tot_self;
 #pragma unroll
       for (int d = 1; d < kUPS; d <<= 1) stage_bytes += __shfl_xor_sync(0xFFFFFFFFu, stage_bytes, d);
-#if ZS_EARLY
-      uint32_t stage_pbytes = valid ? (has_b ? 3072u : 1536u) : 0u;
-#pragma unroll
-      for (int d = 1; d < kUPS; d <<= 1) stage_pbytes += __shfl_xor_sync(0xFFFFFFFFu, stage_pbytes, d);
-#else
-      const uint32_t stage_pbytes = 0u;
-#endif
       // runs of same-band units inside the quad: a run starts at qi == 0 or on a band change
       const uint32_t band_prev = __shfl_up_sync(0xFFFFFFFFu, band, 1);
       const bool run_start = valid && (qi == 0 || band_prev != band);
@@ -359,13 +302,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         __syncwarp();
         if (mine && qi == 0 && stale) mbar_arrive(&bars->full_c[slot]);
-#if ZS_EARLY
-        const bool early = st < nearly && !(p.dbg & 8);   // plane slices already requested
-#else
-        const bool early = false;
-#endif
         if (mine && qi == 0 && !stale) {
-          mbar_arrive_expect_tx(&bars->full_c[slot], early ? stage_bytes - stage_pbytes : stage_bytes);  // release: header visible
+          mbar_arrive_expect_tx(&bars->full_c[slot], stage_bytes);  // release: header visible
           trace_ev(p.trace, it, 0);
         }
         __syncwarp();
@@ -375,21 +313,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint8_t* Hr = planes + kStagePlanes;   // [H a | H b | L a | L b]
           const uint32_t pb = nrun * 512u;
           const uint32_t po = (uint32_t)qi * 512u;
-          if (!early) {
-            bulk_g2s(planes + 0 * (kUPS * 512) + po, p.b1 + (size_t)bta * 64, pb, fb, pol);
-            bulk_g2s(planes + 1 * (kUPS * 512) + po, p.b2 + (size_t)bta * 64, pb, fb, pol);
-            bulk_g2s(planes + 2 * (kUPS * 512) + po, p.b3 + (size_t)bta * 64, pb, fb, pol);
-          }
+          bulk_g2s(planes + 0 * (kUPS * 512) + po, p.b1 + (size_t)bta * 64, pb, fb, pol);
+          bulk_g2s(planes + 1 * (kUPS * 512) + po, p.b2 + (size_t)bta * 64, pb, fb, pol);
+          bulk_g2s(planes + 2 * (kUPS * 512) + po, p.b3 + (size_t)bta * 64, pb, fb, pol);
           if (e_h1a > h0a) bulk_g2s(Hr + oha, p.h + h0a, e_h1a - h0a, fb, pol);
           if (e_l1a > l0a)
             bulk_g2s(Hr + 2 * capH + ola, reinterpret_cast<const uint8_t*>(p.l) + l0a, e_l1a - l0a, fb, pol);
           if (has_b) {
             const size_t btb = (size_t)bta + nbc;
-            if (!early) {
-              bulk_g2s(planes + kBtPlaneStride + 0 * (kUPS * 512) + po, p.b1 + btb * 64, pb, fb, pol);
-              bulk_g2s(planes + kBtPlaneStride + 1 * (kUPS * 512) + po, p.b2 + btb * 64, pb, fb, pol);
-              bulk_g2s(planes + kBtPlaneStride + 2 * (kUPS * 512) + po, p.b3 + btb * 64, pb, fb, pol);
-            }
+            bulk_g2s(planes + kBtPlaneStride + 0 * (kUPS * 512) + po, p.b1 + btb * 64, pb, fb, pol);
+            bulk_g2s(planes + kBtPlaneStride + 1 * (kUPS * 512) + po, p.b2 + btb * 64, pb, fb, pol);
+            bulk_g2s(planes + kBtPlaneStride + 2 * (kUPS * 512) + po, p.b3 + btb * 64, pb, fb, pol);
             if (e_h1b > h0b) bulk_g2s(Hr + capH + ohb, p.h + h0b, e_h1b - h0b, fb, pol);
             if (e_l1b > l0b)
               bulk_g2s(Hr + 2 * capH + capL + olb, reinterpret_cast<const uint8_t*>(p.l) + l0b, e_l1b - l0b, fb,
