@@ -51,7 +51,20 @@ for cta in range(4):
                 rows.append(r[2 + q] - r[11 + q])
             if u + 4 < 128 and r[2 + q] and t[cta, u + 4][7 + q]:
                 gap.append(t[cta, u + 4][7 + q] - r[2 + q])
-for name, d in (("scan+afree (dr->as)", scan), ("rows (as->dq)", rows), ("next unit wait (dq->dr')", gap)):
+# (round 2 loop: the data wait of unit u + 4 happens between the two row passes of unit u, so
+# dr(u + 4) < dq(u); the unit period per warp is as(u + 4) - as(u), the gap dq(u) -> as(u + 4)
+# is the publish + afree wait)
+period, gap2 = [], []
+for cta in range(4):
+    for u in range(124):
+        r, n = t[cta, u], t[cta, u + 4]
+        for q in range(4):
+            if r[11 + q] and n[11 + q]:
+                period.append(n[11 + q] - r[11 + q])
+            if r[2 + q] and n[11 + q]:
+                gap2.append(n[11 + q] - r[2 + q])
+for name, d in (("scan+afree (dr->as)", scan), ("rows (as->dq)", rows), ("next unit wait (dq->dr')", gap),
+                ("unit period (as->as')", period), ("publish+afree (dq->as')", gap2)):
     if d:
         print("%-26s cycles: mean %6.0f  p10 %6.0f  p50 %6.0f  p90 %6.0f" % (name, np.mean(d), np.percentile(d, 10),
                                                                             np.percentile(d, 50), np.percentile(d, 90)))
