@@ -188,8 +188,11 @@ extern "C" zs_status zs_decompress(const zs_tensor* w, uint16_t* out, int64_t ld
   return ZS_OK;
 }
 
+#ifndef ZS_UPS
+#define ZS_UPS 4   // must match zs_gemm.cu (units per ring stage)
+#endif
 #ifndef ZS_XTILES_MAX
-#define ZS_XTILES_MAX 12   // X tiles in the ring at most (L2-sourced; 3 stages of 4 units)
+#define ZS_XTILES_MAX (ZS_UPS == 4 ? 12 : 15)   // X tiles in the ring at most (L2-sourced; 3 stages)
 #endif
 
 // split-K region: fp32 partials [min(M,256)][N] + per-band counters (zero between calls)
@@ -323,6 +326,9 @@ static zs_status gemm_core(const uint16_t* x, int64_t ldx, const zs_tensor* w, u
       if (base + c * cs + pr[1] * xs > budget) continue;
       *nc = c;
       *nx = (uint32_t)std::min<size_t>({(size_t)zs::gemm_max_xslots(), (size_t)ZS_XTILES_MAX, (budget - base - c * cs) / xs});
+      // whole stages of X tiles when the ring holds at least two (stage mode)
+      const uint32_t ups = (uint32_t)zs::gemm_units_per_stage();
+      if (ups != 4 && *nx >= 2 * ups) *nx -= *nx % ups;
       return true;
     }
     return false;
@@ -356,7 +362,7 @@ static zs_status gemm_core(const uint16_t* x, int64_t ldx, const zs_tensor* w, u
     p.n_acc = (2u * p.acc_cols + 2u * 32u * (uint32_t)zs::gemm_units_per_stage() <= 512u) ? 2u : 1u;
     uint32_t na = (512u - p.n_acc * p.acc_cols) / 32u;
     na = std::min<uint32_t>(na, (uint32_t)zs::gemm_max_aslots());
-    p.n_aslots = na - na % 4;
+    p.n_aslots = na - na % (uint32_t)zs::gemm_units_per_stage();
     auto magic = [](uint32_t d) { return d <= 1u ? 0u : (uint32_t)((1ull << 32) / d + 1ull); };
     p.cdiv_magic = magic(p.n_cslots);
     p.adiv_magic = magic(p.n_aslots / (uint32_t)zs::gemm_units_per_stage());

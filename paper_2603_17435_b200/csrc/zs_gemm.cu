@@ -51,14 +51,17 @@ namespace zs {
 #define ZS_BACKOFF_DEC 32     // ns between barrier probes of a decoder warp
 #endif
 constexpr uint32_t kLutBytes = 4096u;   // selector table (a second table of fallback selectors measured 4% slower)
+#ifndef ZS_UPS
+#define ZS_UPS 4   // units per ring stage = decoder warps per TMEM lane quarter
+#endif
 #ifndef ZS_DEC_PER_Q
-#define ZS_DEC_PER_Q 4   // decoder warps per TMEM lane quarter (static unit assignment, see below)
+#define ZS_DEC_PER_Q ZS_UPS   // decoder warps per TMEM lane quarter (static unit assignment, see below)
 #endif
 constexpr int kDecPerQuarter = ZS_DEC_PER_Q;
 // one decoder warp per unit of a stage: with more warps than units per stage a warp's next unit
 // can sit two stages ahead of its current one (measured: D = 5 deadlocks on the 3-slot
 // compressed ring at M = 200 and is 25% slower where it completes, r02 it6)
-static_assert(kDecPerQuarter == 4, "the static unit assignment assumes one decoder warp per unit of a stage");
+static_assert(kDecPerQuarter == ZS_UPS, "the static unit assignment assumes one decoder warp per unit of a stage");
 constexpr int kWarpDec0 = 0;                       // warps 0..4D-1: decoders (lane quarter = warp % 4)
 constexpr int kWarpEpi0 = 4 * kDecPerQuarter;      // 4 epilogue warps (TMEM lane quarters)
 constexpr int kWarpAlloc = kWarpEpi0 + 4;
@@ -66,10 +69,10 @@ constexpr int kWarpProdX = kWarpEpi0 + 5;
 constexpr int kWarpProdC = kWarpEpi0 + 6;
 constexpr int kWarpMma = kWarpEpi0 + 7;            // highest id: first pick of its SMSP's arbiter
 constexpr int kGemmThreads = 32 * (kWarpEpi0 + 8);  // 768 at D = 4 (80 registers per thread)
-constexpr int kUPS = 4;                            // units per ring stage
+constexpr int kUPS = ZS_UPS;                       // units per ring stage
 constexpr int kMaxCSlots = 8;
 constexpr int kMaxXSlots = 16;
-constexpr int kMaxASlots = 12;
+constexpr int kMaxASlots = 3 * kUPS;
 constexpr uint32_t kStageMeta = 128;               // see the stage header layout below
 // planes of a stage: [BlockTile row a | b][B1 | B2 | B3][unit][512 B]; row b's planes start
 // 32 B past a multiple of 128 B, so the two halves of a decoder warp (rows of BlockTile a and b
@@ -243,9 +246,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const ulonglong2* off2 = reinterpret_cast<const ulonglong2*>(p.offsets);
     const int quad = lane / kUPS, qi = lane % kUPS;   // lane group of a stage / unit in it
     uint32_t slot = 0, eph = 1;   // ring slot / empty-barrier parity of the next stage
-    for (int b0 = 0; b0 < nunits; b0 += 32) {
+    constexpr int kBatch = (32 / kUPS) * kUPS;   // units per batch: whole stages
+    for (int b0 = 0; b0 < nunits; b0 += kBatch) {
       const int it = b0 + lane;
-      const bool valid = it < nunits;
+      const bool valid = it < nunits && lane < kBatch;
       const uint32_t kk = kc0 + (uint32_t)it;
       const uint32_t band = band0 + kk / nbc, kc = kk % nbc;
       const uint32_t bta = 2u * band * nbc + kc;
@@ -270,9 +274,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       // pha.. are now inclusive; exclusive = inclusive - own size
       const uint32_t oha = pha - (h1a - h0a), ohb = phb - (h1b - h0b), ola = pla - (l1a - l0a), olb = plb - (l1b - l0b);
+#if ZS_UPS == 4
       uint32_t stage_bytes = tot_self;
 #pragma unroll
       for (int d = 1; d < kUPS; d <<= 1) stage_bytes += __shfl_xor_sync(0xFFFFFFFFu, stage_bytes, d);
+#else
+      // (not a power of two: inclusive scan inside the group, total from its last lane)
+      uint32_t stage_bytes = tot_self;
+#pragma unroll
+      for (int d = 1; d < kUPS; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, stage_bytes, d);
+        if (qi >= d) stage_bytes += t;
+      }
+      stage_bytes = __shfl_sync(0xFFFFFFFFu, stage_bytes, (quad * kUPS + kUPS - 1) & 31);
+#endif
       // runs of same-band units inside the quad: a run starts at qi == 0 or on a band change
       const uint32_t band_prev = __shfl_up_sync(0xFFFFFFFFu, band, 1);
       const bool run_start = valid && (qi == 0 || band_prev != band);
@@ -287,7 +302,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t e_h1a = __shfl_sync(0xFFFFFFFFu, h1a, rend), e_l1a = __shfl_sync(0xFFFFFFFFu, l1a, rend);
       const uint32_t e_h1b = __shfl_sync(0xFFFFFFFFu, h1b, rend), e_l1b = __shfl_sync(0xFFFFFFFFu, l1b, rend);
       const uint32_t nrun = (uint32_t)(rend - lane + 1);
-      const int st_hi = min(nstages, (b0 + 32) / kUPS);
+      const int st_hi = min(nstages, (b0 + kBatch) / kUPS);
       for (int st = b0 / kUPS; st < st_hi; ++st, slot = (slot + 1 == S_c) ? 0u : slot + 1u, eph ^= (slot == 0)) {
         mbar_wait(&bars->empty_c[slot], eph, ZS_BACKOFF_CTRL);
         uint8_t* cs = cslots + (size_t)slot * p.cslot_bytes;
