@@ -21,7 +21,10 @@ namespace {
 thread_local int g_last_launches = 0;
 unsigned long long* g_trace = nullptr;  // debug: set by zs_debug_set_trace
 uint32_t g_dbg = 0;                     // debug: experiment flags (zs_debug_set_flags)
-uint32_t g_max_cslots = 16;             // ring depth cap (tunable via zs_debug_set_ring)
+#ifndef ZS_RING_CAP
+#define ZS_RING_CAP 16
+#endif
+uint32_t g_max_cslots = ZS_RING_CAP;    // ring depth cap (tunable via zs_debug_set_ring)
 int64_t g_large_m = -1;                 // forced decoupled-path threshold (zs_debug_set_large_m), -1 = per shape
 
 // cuBLAS handle of the decoupled prefill path: one per (host thread, device), created on
