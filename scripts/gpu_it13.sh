@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+AB_LAYERS=L8B.GateUp,L8B.Down,L8B.QKV,L8B.O AB_MS=1,32 bash scripts/gpu_ab.sh it13 u3
+AB_LAYERS=L8B.GateUp AB_MS=128,256 bash scripts/gpu_ab.sh it13b u3
