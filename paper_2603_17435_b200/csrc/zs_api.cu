@@ -194,6 +194,10 @@ extern "C" zs_status zs_decompress(const zs_tensor* w, uint16_t* out, int64_t ld
 #ifndef ZS_UPS
 #define ZS_UPS 4   // must match zs_gemm.cu (units per ring stage)
 #endif
+#ifndef ZS_SPLIT3
+#define ZS_SPLIT3 2   // > 0: prefer 3 compressed stages with that many X tiles over 2 stages with 4
+                      // (2: M = 129..256 run 3 stages + 2 X tiles; 8B GateUp M = 144 / 256: 108.5 / 122.3 -> 93.0 / 111.5 us)
+#endif
 #ifndef ZS_XTILES_MAX
 #define ZS_XTILES_MAX (ZS_UPS == 4 ? 12 : 15)   // X tiles in the ring at most (L2-sourced; 3 stages)
 #endif
@@ -323,7 +327,11 @@ static zs_status gemm_core(const uint16_t* x, int64_t ldx, const zs_tensor* w, u
     const uint32_t cmax = std::min<uint32_t>((uint32_t)zs::gemm_max_cslots(), g_max_cslots);
     // preference: 3 compressed stages with >= 4 X tiles (measured best at small M; a 4th
     // stage measured no change), then 2 stages with >= 4 tiles, then 2 with >= 2 tiles
+#if ZS_SPLIT3
+    static const uint32_t pref[][2] = {{3, 4}, {3, ZS_SPLIT3}, {2, 4}, {2, 2}, {1, 2}};
+#else
     static const uint32_t pref[][2] = {{3, 4}, {2, 4}, {2, 2}, {1, 2}};
+#endif
     for (const auto& pr : pref) {
       const uint32_t c = std::min(pr[0], cmax);
       if (base + c * cs + pr[1] * xs > budget) continue;
