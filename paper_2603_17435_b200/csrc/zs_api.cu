@@ -326,7 +326,8 @@ static zs_status gemm_core(const uint16_t* x, int64_t ldx, const zs_tensor* w, u
     const size_t cs = p.cslot_bytes;
     const uint32_t cmax = std::min<uint32_t>((uint32_t)zs::gemm_max_cslots(), g_max_cslots);
     // preference: 3 compressed stages with >= 4 X tiles (measured best at small M; a 4th
-    // stage measured no change), then 2 stages with >= 4 tiles, then 2 with >= 2 tiles
+    // stage measured no change), then 3 stages with >= ZS_SPLIT3 tiles (the 129..256-token
+    // chunks: a 2-stage ring does not hide HBM there), then 2 stages with >= 4 / >= 2 tiles
 #if ZS_SPLIT3
     static const uint32_t pref[][2] = {{3, 4}, {3, ZS_SPLIT3}, {2, 4}, {2, 2}, {1, 2}};
 #else
